@@ -1,0 +1,288 @@
+"""Parity of the device path (through the C ABI) with the reference.
+
+MIRROR arithmetic reproduces the reference's IEEE operation sequence, so its
+terms, range partials and totals are compared BIT-EXACTLY with fixtures
+produced by the reference itself (tests/golden) and with the C oracle.
+FAST arithmetic is compared within the stated tolerances.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import bits, has_gpu, load_golden, random_symmetric, rel_err
+from oracle import bruteforce as BF
+from oracle import oracle as O
+from paper_1805_12498_b200 import engine, kernels, workloads
+from paper_1805_12498_b200.errors import DegenerateHessenberg, OddDimension
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")]
+
+
+# ------------------------------------------------------------------ golden, bit-exact
+
+def test_terms_mirror_bit_exact_vs_reference():
+    g = load_golden("terms.npz")
+    for name, case in g.items():
+        loops = bool(case["loops"])
+        at, dg, nh = engine._prepare(case["A"], loops)
+        for backend in (1, 0):
+            vals, st = kernels.terms(at, dg, nh, case["masks"], backend, loops, arith="mirror")
+            assert np.array_equal(st, case[f"status_b{backend}"]), name
+            same = bits(vals) == bits(case[f"terms_b{backend}"])
+            assert same.all(), f"{name} b{backend}: {np.count_nonzero(~same)} words differ"
+
+
+def test_range_partials_mirror_bit_exact_vs_reference():
+    g = load_golden("ranges.npz")
+    for name, case in g.items():
+        loops = bool(case["loops"])
+        at, dg, nh = engine._prepare(case["A"], loops)
+        nr = min((1 << nh) - 1, 512)
+        for backend in (1, 0):
+            sums, fails = kernels.sum_subsets_det(at, dg, nh, backend, loops, 1, nr, arith="mirror")
+            assert (bits(sums) == bits(case[f"partials_b{backend}"])).all(), f"{name} b{backend}"
+            assert np.array_equal(fails, case[f"fails_b{backend}"])
+            fs, _ = kernels.sum_subsets_fast(at, dg, nh, backend, loops, 3, nr, arith="mirror")
+            assert (bits(fs) == bits(case[f"fast3_b{backend}"])).all(), f"{name} fast b{backend}"
+
+
+def test_public_api_bit_identical_to_reference_results():
+    g = load_golden("ranges.npz")
+    for name, case in g.items():
+        loops = bool(case["loops"])
+        f = engine.loop_hafnian if loops else engine.hafnian
+        for backend, bname in ((1, "charpoly"), (0, "spectral")):
+            got = f(case["A"], backend=bname)
+            assert got == complex(case[f"result_b{backend}"]), (name, bname)
+
+
+def test_cfg3_matching_count_rounds_like_reference():
+    """cfg3 (n=40 ER graph): the mirror result equals the reference's float result,
+    so rounding it gives the reference's integer; the exact count differs from both
+    (the float formula cannot resolve 3.1e17 > 2^53, SURVEY.md finding 4)."""
+    g = load_golden("ranges.npz")["cfg3"]
+    got = engine.hafnian(g["A"], backend="charpoly")
+    assert got == complex(g["result_b1"])
+    assert round(got.real) == round(complex(g["result_b1"]).real)
+    exact = 308544357990268074
+    assert abs(got.real - exact) / exact < 1e-5
+
+
+def test_n52_range_mirror_bit_exact():
+    g = load_golden("range_n52.npz")
+    for name, case in g.items():
+        at, dg, nh = engine._prepare(case["A"], False)
+        for backend in (1, 0):
+            key = f"partials_b{backend}"
+            if key not in case:
+                continue
+            sums, fails = kernels.sum_mask_range(at, dg, nh, 0, 1 << 20, 512, backend, False,
+                                                 arith="mirror")
+            assert (bits(sums) == bits(case[key])).all(), (name, backend)
+            assert engine.tree_reduce(sums) == complex(case[f"result_b{backend}"])
+
+
+def test_batch_equals_single_calls():
+    g = load_golden("ranges.npz")
+    mats = [g[f"cfg1s{s}"]["A"] for s in range(4)]
+    res = engine.hafnian_batch(mats, backend="charpoly")
+    for s in range(4):
+        assert res[s] == complex(g[f"cfg1s{s}"]["result_b1"])
+    res0 = engine.hafnian_batch(mats, backend="spectral")
+    for s in range(4):
+        assert res0[s] == complex(g[f"cfg1s{s}"]["result_b0"])
+
+
+def test_powertraces_mirror_bit_exact():
+    g = load_golden("powertraces.npz")
+    for q, case in g.items():
+        b, K = case["b"], int(case["K"])
+        t, ok = kernels.power_traces_charpoly(b, K)
+        assert ok == bool(case["charpoly_ok"])
+        assert (bits(t) == bits(case["charpoly_traces"])).all(), q
+        assert (bits(kernels.charpoly_coefficients(b)) == bits(case["coeffs"])).all(), q
+        ts, _, conv = kernels.power_traces_spectral(b, K)
+        assert conv == bool(case["spectral_conv"])
+        assert (bits(ts) == bits(case["spectral_traces"])).all(), q
+
+
+# ------------------------------------------------------------------ oracle, bit-exact
+
+@pytest.mark.parametrize("n,loops,seed", [(2, False, 1), (6, True, 2), (16, False, 3),
+                                          (18, True, 4), (24, False, 5), (28, True, 6)])
+def test_random_vs_oracle_bit_exact(n, loops, seed):
+    A = random_symmetric(n, seed)
+    at, dg, nh = engine._prepare(A, loops)
+    nr = min((1 << nh) - 1, 512)
+    for backend in (1, 0):
+        sums, fails = kernels.sum_subsets_det(at, dg, nh, backend, loops, 1, nr)
+        ref, rf = O.sum_subsets_det(at, dg, nh, backend, loops, 8, nr)
+        assert (bits(sums) == bits(ref)).all()
+        assert np.array_equal(fails, rf)
+
+
+def test_sharded_range_lists_reassemble_bit_exact():
+    A = workloads.cfg0()
+    at, dg, nh = engine._prepare(A, False)
+    full, _ = kernels.sum_subsets_det(at, dg, nh, 1, False, 1, 512)
+    from paper_1805_12498_b200 import costmodel
+
+    for k in (2, 3, 8):
+        shards = costmodel.lpt_shards(costmodel.range_costs(nh, 512), k)
+        got = np.zeros(512, np.complex128)
+        for sh in shards:
+            s, f = kernels.sum_range_list(at, dg, nh, 512, sh, 1, False)
+            got[sh] = s
+        assert (bits(got) == bits(full)).all()
+
+
+# ------------------------------------------------------------------ reference test KATs
+# (the hot-path rows of SURVEY.md section 4, ported to the device API)
+
+def test_empty_and_odd():
+    assert engine.hafnian(np.zeros((0, 0))) == 1
+    with pytest.raises(OddDimension):
+        engine.hafnian(np.zeros((3, 3)))
+    with pytest.raises(OddDimension):
+        engine.loop_hafnian(np.eye(5))
+
+
+def test_single_pair_and_4x4():
+    a = 0.7 - 0.2j
+    assert rel_err(engine.hafnian(np.array([[0, a], [a, 0]])), a) < 1e-14
+    b = random_symmetric(4, 100)
+    np.fill_diagonal(b, 0)
+    expected = b[0, 1] * b[2, 3] + b[0, 2] * b[1, 3] + b[0, 3] * b[1, 2]
+    assert rel_err(engine.hafnian(b), expected) < 1e-12
+
+
+def test_diagonal_ignored_bitwise():
+    a = random_symmetric(6, 101)
+    b = a.copy()
+    np.fill_diagonal(b, 0)
+    assert engine.hafnian(a) == engine.hafnian(b)
+
+
+@pytest.mark.parametrize("arith", ["mirror", "fast"])
+def test_complete_graph_double_factorial(arith):
+    a = np.ones((20, 20), dtype=complex)
+    np.fill_diagonal(a, 0)
+    for backend in ("charpoly", "spectral"):
+        assert rel_err(engine.hafnian(a, backend=backend, arith=arith), BF.double_factorial(19)) < 1e-9
+
+
+@pytest.mark.parametrize("m", [2, 3, 4, 5])
+def test_bipartite_equals_permanent(m):
+    rng = np.random.default_rng(m + 200)
+    w = rng.uniform(-1, 1, (m, m)) + 1j * rng.uniform(-1, 1, (m, m))
+    assert rel_err(engine.hafnian(BF.bipartite_embedding(w)), BF.permanent_ryser(w)) < 1e-9
+
+
+@pytest.mark.parametrize("n", [2, 4, 6, 8, 10])
+@pytest.mark.parametrize("arith", ["mirror", "fast"])
+def test_random_vs_bruteforce(n, arith):
+    a = random_symmetric(n, n + 300)
+    np.fill_diagonal(a, 0)
+    assert rel_err(engine.hafnian(a, arith=arith), BF.hafnian_bruteforce(a)) < 1e-10
+    b = random_symmetric(n, n + 400)
+    assert rel_err(engine.loop_hafnian(b, arith=arith), BF.loop_hafnian_bruteforce(b)) < 1e-10
+
+
+def test_loop_hafnian_kats():
+    assert rel_err(engine.loop_hafnian(np.ones((10, 10))), BF.telephone(10)) < 1e-9
+    d = np.array([1.5, -2.0, 0.5 + 1j, 3.0, -0.25, 2.0 - 1j])
+    assert rel_err(engine.loop_hafnian(np.diag(d)), d.prod()) < 1e-12
+    a = random_symmetric(10, 103)
+    np.fill_diagonal(a, 0)
+    assert engine.loop_hafnian(a) == engine.hafnian(a)
+
+
+@pytest.mark.parametrize("n", [4, 6, 8, 10])
+def test_matching_count_identity(n):
+    rng = np.random.default_rng(n + 50)
+    adj = np.triu((rng.uniform(size=(n, n)) < 0.6).astype(int), 1)
+    adj = adj + adj.T
+    count = BF.matching_count(adj)
+    lhaf = engine.loop_hafnian(adj.astype(complex) + np.eye(n))
+    assert round(lhaf.real) == count
+    assert abs(lhaf - count) <= 1e-9 * max(1, count)
+
+
+@pytest.mark.parametrize("mu", [0.5, 2.0, 3 + 4j])
+@pytest.mark.parametrize("n", [4, 8, 12])
+def test_homogeneity(mu, n):
+    a = random_symmetric(n, n + 500)
+    np.fill_diagonal(a, 0)
+    assert rel_err(engine.hafnian(mu * a), mu ** (n // 2) * engine.hafnian(a)) < 1e-10
+
+
+def test_subset_terms():
+    a = 1.3 + 0.4j
+    assert rel_err(engine.subset_term(np.array([[0, a], [a, 0]]), 1), a) < 1e-14
+    k4 = np.ones((4, 4), dtype=complex)
+    np.fill_diagonal(k4, 0)
+    assert rel_err(sum(engine.subset_term(k4, m) for m in range(1, 4)), 3) < 1e-12
+    with pytest.raises(ValueError):
+        engine.subset_term(np.zeros((2, 2)), 0)
+    with pytest.raises(ValueError):
+        engine.subset_term(np.zeros((2, 2)), 2)
+
+
+def test_deterministic_across_devices_and_repeats():
+    a = np.ones((20, 20), dtype=complex)
+    np.fill_diagonal(a, 0)
+    results = {engine.hafnian(a, threads=t) for t in (1, 2, 4, 8)}
+    assert len(results) == 1
+    b = random_symmetric(12, 14)
+    assert engine.hafnian(b) == engine.hafnian(b)
+
+
+def test_concurrent_calls():
+    import threading
+
+    mats = [random_symmetric(10, 600 + i) for i in range(4)]
+    expected = [engine.hafnian(m) for m in mats]
+    out = [None] * 4
+
+    def work(i):
+        out[i] = engine.hafnian(mats[i], threads=2)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert out == expected
+
+
+def test_sweep_cap_zero_raises(monkeypatch):
+    from paper_1805_12498_b200.errors import EigensolverNoConvergence
+
+    monkeypatch.setattr(kernels, "SWEEP_CAP_MULT", 0)
+    a = random_symmetric(8, 15)
+    np.fill_diagonal(a, 0)
+    with pytest.raises(EigensolverNoConvergence):
+        engine.hafnian(a)
+
+
+def test_nonfinite_input_statuses_match_oracle():
+    a = random_symmetric(8, 16)
+    a[0, 1] = a[1, 0] = np.inf
+    at, dg, nh = engine._prepare(a, False)
+    for backend in (1, 0):
+        _, fails = kernels.sum_subsets_det(at, dg, nh, backend, False, 1, 15)
+        _, rf = O.sum_subsets_det(at, dg, nh, backend, False, 1, 15)
+        assert np.array_equal(fails, rf)
+    if O.sum_subsets_det(at, dg, nh, 1, False, 1, 15)[1].max() == 2:
+        with pytest.raises(DegenerateHessenberg):
+            engine.hafnian(a, backend="charpoly")
+
+
+# ------------------------------------------------------------------ fast arithmetic
+
+@pytest.mark.parametrize("cfg,tol", [("cfg0", 1e-11), ("cfg1s0", 1e-9)])
+def test_fast_arith_within_tolerance(cfg, tol):
+    g = load_golden("ranges.npz")[cfg]
+    got = engine.hafnian(g["A"], backend="charpoly", arith="fast")
+    assert rel_err(got, complex(g["result_b1"])) < tol

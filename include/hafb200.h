@@ -116,11 +116,19 @@ int hafb_sum_range_list(const double* atilde, const double* diag, int n_half, in
                         const int32_t* ranges, int count, int backend, int include_loops,
                         int cap_mult, int arith, int device, double* partials, int64_t* fails);
 size_t hafb_range_list_workspace_bytes(int n_half, int n_ranges, int count);
+/* Device-resident range-list variant: d_atilde / d_diag / d_partials / d_fails and the
+ * workspace are device pointers, `ranges` is a HOST array (the shard plan).  If
+ * terms_done_event (a cudaEvent_t) is non-null it is recorded on `stream` between the
+ * subset-term kernels and the range reduction (kernel-level timing). */
 int hafb_sum_range_list_async(const double* d_atilde, const double* d_diag, int n_half,
-                              int n_ranges, const int32_t* d_ranges, int count, int backend,
+                              int n_ranges, const int32_t* ranges, int count, int backend,
                               int include_loops, int cap_mult, int arith, void* d_workspace,
                               size_t workspace_bytes, double* d_partials, int64_t* d_fails,
-                              void* stream);
+                              void* stream, void* terms_done_event);
+
+/* Calibration: FP64 FMA throughput of `device` measured by a DFMA-saturating probe
+ * kernel (the roofline denominator for the subset-term kernels).  tflops = 2 flop/DFMA. */
+int hafb_fp64_peak(int device, double* tflops, double* ms);
 
 /* Kernel launches issued by the calling thread since the last reset (the bench's
  * gpu_launches claim). */

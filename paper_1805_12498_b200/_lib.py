@@ -49,9 +49,10 @@ SIGNATURES = {
     "hafb_sum_range_list": (_int, [_dp, _dp, _int, _int, _i32p, _int, _int, _int, _int, _int, _int,
                                    _dp, _i64p]),
     "hafb_range_list_workspace_bytes": (_size, [_int, _int, _int]),
-    "hafb_sum_range_list_async": (_int, [_vp, _vp, _int, _int, _vp, _int, _int, _int, _int, _int,
-                                         _vp, _size, _vp, _vp, _vp]),
+    "hafb_sum_range_list_async": (_int, [_vp, _vp, _int, _int, _i32p, _int, _int, _int, _int,
+                                         _int, _vp, _size, _vp, _vp, _vp, _vp]),
     "hafb_launch_count": (_i64, [_int]),
+    "hafb_fp64_peak": (_int, [_int, _dp, _dp]),
 }
 
 

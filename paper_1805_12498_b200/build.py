@@ -1,9 +1,11 @@
 """In-tree build of the CUDA C-ABI library (sm_100a only).
 
-    python -m paper_1805_12498_b200.build
+    python -m paper_1805_12498_b200.build [--force] [-v]
 
-produces ``paper_1805_12498_b200/libhafb200.so``.  The .so is git-ignored but
-travels to the GPU box with the repo snapshot.
+Compiles csrc/hafb200.cu (ABI, shared-memory kernels, reductions) and one
+object per register-kernel size (csrc/fast_inst.cu with -DHAFB_S=S) in
+parallel, then links ``paper_1805_12498_b200/libhafb200.so``.  The .so is
+git-ignored but travels to the GPU box with the repo snapshot.
 """
 
 from __future__ import annotations
@@ -12,13 +14,15 @@ import os
 import shutil
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
+OBJ = os.path.join(os.environ.get("HAFB200_BUILD_DIR", "/tmp/hafb200_build"))
 LIB = os.path.join(PKG, "libhafb200.so")
-SOURCES = ["hafb200.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FAST_SIZES = list(range(2, 49, 2))  # kFastSMax = 48 (csrc/fast_launch.h)
 
 
 def nvcc() -> str:
@@ -29,7 +33,7 @@ def nvcc() -> str:
 
 
 def _deps():
-    out = [os.path.join(REPO, "include", "hafb200.h")]
+    out = [os.path.join(REPO, "include", "hafb200.h"), os.path.abspath(__file__)]
     for f in os.listdir(CSRC):
         if f.endswith((".cu", ".cuh", ".h")):
             out.append(os.path.join(CSRC, f))
@@ -43,15 +47,48 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def _flags(verbose):
+    f = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
+         "-I", os.path.join(REPO, "include")]
+    if verbose:
+        f.append("-Xptxas=-v")
+    return f
+
+
+def _units():
+    units = [("hafb200.o", os.path.join(CSRC, "hafb200.cu"), [])]
+    for s in FAST_SIZES:
+        units.append((f"fast_{s:02d}.o", os.path.join(CSRC, "fast_inst.cu"), [f"-DHAFB_S={s}"]))
+    return units
+
+
+def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -> str:
     if not force and up_to_date():
         return LIB
-    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "--shared", "-Xcompiler", "-fPIC",
-           "-Xcompiler", "-O2", "-I", os.path.join(REPO, "include"), "-o", LIB + ".tmp",
-           *[os.path.join(CSRC, s) for s in SOURCES]]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    subprocess.run(cmd, check=True)
+    os.makedirs(OBJ, exist_ok=True)
+    cc = nvcc()
+    flags = _flags(verbose)
+
+    def compile_one(u):
+        obj, src, extra = u
+        out = os.path.join(OBJ, obj)
+        r = subprocess.run([cc, *flags, *extra, "-c", src, "-o", out], capture_output=True, text=True)
+        return obj, r
+
+    jobs = jobs or max(1, (os.cpu_count() or 2))
+    failed = []
+    with ThreadPoolExecutor(max_workers=jobs) as ex:
+        for obj, r in ex.map(compile_one, _units()):
+            if verbose and (r.stdout or r.stderr):
+                sys.stderr.write(f"== {obj}\n{r.stdout}{r.stderr}")
+            if r.returncode != 0:
+                failed.append((obj, r.stderr))
+    if failed:
+        for obj, err in failed:
+            sys.stderr.write(f"== {obj} FAILED\n{err}\n")
+        raise RuntimeError(f"nvcc failed for {[f[0] for f in failed]}")
+    objs = [os.path.join(OBJ, u[0]) for u in _units()]
+    subprocess.run([cc, *ARCH, "--shared", "-o", LIB + ".tmp", *objs], check=True)
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -1,0 +1,73 @@
+// enumerate.cuh -- size-class enumeration of pair subsets.
+//
+// The reference walks masks in numeric order (_numba.py:375); the cost of a
+// mask grows like popcount^3, so a warp that mixes popcounts diverges and a
+// fixed range split is unbalanced (SURVEY.md H2 / finding 5).  Here every
+// kernel launch handles ONE popcount class m: item rho of the class maps to
+// the rho-th mask of popcount m inside a list of mask segments, by colex
+// unranking (combinatorial number system).  Terms are written to the buffer
+// slot of their mask, so the order-defined reduction afterwards is unchanged.
+#pragma once
+
+#include <stdint.h>
+
+namespace hafb {
+
+struct Seg {
+    unsigned long long lo, hi;  // masks [lo, hi)
+    long long out_off;          // buffer index of mask x is out_off + (x - lo)
+};
+
+// Items of one popcount class over a segment list (and over `batch` problems).
+struct ClassItems {
+    const unsigned long long* binom;    // [33][33] table of C(b, p)
+    const Seg* segs;
+    const long long* prefix;            // nseg+1: # class-m masks before segment s
+    const unsigned long long* base;     // nseg: # class-m integers below segs[s].lo
+    int nseg;
+    int m;
+    int D;
+    long long per_problem;              // = prefix[nseg]
+    long long n_items;                  // = batch * per_problem
+    long long term_stride;              // buffer offset between problems
+    long long at_stride, dg_stride;     // input offsets between problems (in cd)
+};
+
+// the r-th (0-based) integer with popcount m, bits below D
+__device__ __forceinline__ uint32_t unrank_mask(const unsigned long long* __restrict__ binom,
+                                                unsigned long long r, int m, int D) {
+    uint32_t mask = 0;
+    for (int b = D - 1; b >= 0 && m > 0; --b) {
+        unsigned long long c = __ldg(binom + b * 33 + m);
+        if (r >= c) {
+            mask |= 1u << b;
+            r -= c;
+            --m;
+        }
+    }
+    return mask;
+}
+
+struct ItemRef {
+    uint32_t mask;
+    long long problem;
+    long long out;  // buffer index (including the problem offset)
+};
+
+__device__ __forceinline__ ItemRef resolve_item(const ClassItems& ci, long long item) {
+    ItemRef r;
+    r.problem = item / ci.per_problem;
+    long long rho = item - r.problem * ci.per_problem;
+    int lo = 0, hi = ci.nseg - 1;
+    while (lo < hi) {  // last s with prefix[s] <= rho
+        int mid = (lo + hi + 1) >> 1;
+        if (ci.prefix[mid] <= rho) lo = mid;
+        else hi = mid - 1;
+    }
+    const Seg sg = ci.segs[lo];
+    r.mask = unrank_mask(ci.binom, ci.base[lo] + (unsigned long long)(rho - ci.prefix[lo]), ci.m, ci.D);
+    r.out = r.problem * ci.term_stride + sg.out_off + (long long)(r.mask - sg.lo);
+    return r;
+}
+
+}  // namespace hafb

@@ -1,0 +1,19 @@
+// fast_launch.h -- host launchers of the register kernels, one translation unit
+// per size S (fast_inst.cu compiled with -DHAFB_S=S) so they build in parallel.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "cplx.cuh"
+#include "enumerate.cuh"
+
+namespace hafb {
+
+constexpr int kFastSMax = 48;  // sizes above run in the shared-memory kernel
+
+// launch fast_term_kernel<S, loops> over the items of one popcount class
+template <int S>
+cudaError_t launch_fast_S(bool loops, const cd* at, const cd* dg, int n_half, const ClassItems& ci,
+                          cd* terms, int8_t* status, cudaStream_t st, int sms);
+
+}  // namespace hafb

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -16,6 +17,7 @@
 #include "cplx.cuh"
 #include "reduce.cuh"
 #include "term_smem.cuh"
+#include "fast_launch.h"
 
 using namespace hafb;
 
@@ -56,7 +58,24 @@ struct Call {
     cudaError_t open(int device) {
         cudaError_t e = cudaSetDevice(device);
         if (e != cudaSuccess) return e;
+        e = keep_pool(device);
+        if (e != cudaSuccess) return e;
         return cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    }
+    // keep freed stream-ordered memory in the device pool across calls (the default
+    // release threshold of 0 hands it back to the driver at every synchronisation)
+    static cudaError_t keep_pool(int device) {
+        static std::once_flag once[64];
+        cudaError_t err = cudaSuccess;
+        if (device < 0 || device >= 64) return cudaErrorInvalidDevice;
+        std::call_once(once[device], [&] {
+            cudaMemPool_t pool;
+            err = cudaDeviceGetDefaultMemPool(&pool, device);
+            if (err != cudaSuccess) return;
+            unsigned long long thr = ~0ull;
+            err = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        });
+        return err;
     }
     template <class T>
     cudaError_t alloc(T** p, size_t bytes) {
@@ -139,19 +158,185 @@ uint64_t std_width(int n_half, int n_ranges) {
     return (nterms + n_ranges - 1) / n_ranges;
 }
 
+// ------------------------------------------------------------------ FAST class path
+// Every popcount class m gets one launch of the register kernel for S = 2m
+// (sizes above kFastSMax fall back to the shared-memory kernel).
+
+unsigned long long g_binom_host[33][33];
+std::once_flag g_binom_once;
+
+void init_binom_host() {
+    for (int b = 0; b <= 32; ++b)
+        for (int p = 0; p <= 32; ++p) {
+            if (p == 0) g_binom_host[b][p] = 1;
+            else if (b == 0) g_binom_host[b][p] = 0;
+            else g_binom_host[b][p] = g_binom_host[b - 1][p - 1] + g_binom_host[b - 1][p];
+        }
+}
+
+// # of integers y in [0, x) with popcount p (x <= 2^32)
+unsigned long long count_below_host(unsigned long long x, int p, int D) {
+    if (p < 0) return 0;
+    unsigned long long total = 0;
+    int ones = 0;
+    for (int b = D; b >= 0; --b) {
+        if ((x >> b) & 1ull) {
+            int need = p - ones;
+            if (need >= 0 && need <= b) total += g_binom_host[b][need];
+            ++ones;
+            if (ones > p) break;
+        }
+    }
+    return total;
+}
+
+// device-side image of the per-class enumeration tables
+struct ClassTables {
+    int D = 0, nseg = 0;
+    std::vector<long long> prefix;            // (D+1) x (nseg+1)
+    std::vector<unsigned long long> base;     // (D+1) x nseg
+    long long count(int m) const { return prefix[(size_t)m * (nseg + 1) + nseg]; }
+};
+
+ClassTables build_tables(int D, const std::vector<Seg>& segs) {
+    std::call_once(g_binom_once, init_binom_host);
+    ClassTables t;
+    t.D = D;
+    t.nseg = (int)segs.size();
+    t.prefix.assign((size_t)(D + 1) * (t.nseg + 1), 0);
+    t.base.assign((size_t)(D + 1) * t.nseg, 0);
+    for (int m = 1; m <= D; ++m) {
+        long long acc = 0;
+        for (int s = 0; s < t.nseg; ++s) {
+            unsigned long long b0 = count_below_host(segs[s].lo, m, D);
+            unsigned long long b1 = count_below_host(segs[s].hi, m, D);
+            t.prefix[(size_t)m * (t.nseg + 1) + s] = acc;
+            t.base[(size_t)m * t.nseg + s] = b0;
+            acc += (long long)(b1 - b0);
+        }
+        t.prefix[(size_t)m * (t.nseg + 1) + t.nseg] = acc;
+    }
+    return t;
+}
+
+template <bool L>
+cudaError_t launch_smem_class(const cd* at, const cd* dg, int n_half, const ClassItems& ci, int cap,
+                              cd* terms, int8_t* status, cudaStream_t st) {
+    const int n = 2 * n_half;
+    size_t per_warp = (size_t)smem_warp_elems(n) * sizeof(cd);
+    int wpb = (int)std::min<size_t>(8, std::max<size_t>(1, (200 * 1024) / per_warp));
+    size_t smem = wpb * per_warp;
+    auto kern = terms_smem_class_kernel<1, L>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int occ = 1;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, wpb * 32, smem);
+    if (e != cudaSuccess) return e;
+    long long want = (ci.n_items + wpb - 1) / wpb;
+    int grid = (int)std::max<long long>(1, std::min(want, (long long)sm_count() * std::max(occ, 1)));
+    kern<<<grid, wpb * 32, smem, st>>>(at, dg, n_half, ci, cap, terms, status);
+    return cudaGetLastError();
+}
+
+template <bool L>
+cudaError_t launch_fast_class(int S, const cd* at, const cd* dg, int n_half, const ClassItems& ci,
+                              int cap, cd* terms, int8_t* status, cudaStream_t st) {
+    const int sms = sm_count();
+    switch (S) {
+#define FC(SS) \
+    case SS: return launch_fast_S<SS>(L, at, dg, n_half, ci, terms, status, st, sms);
+        FC(2) FC(4) FC(6) FC(8) FC(10) FC(12) FC(14) FC(16) FC(18) FC(20) FC(22) FC(24)
+        FC(26) FC(28) FC(30) FC(32) FC(34) FC(36) FC(38) FC(40) FC(42) FC(44) FC(46) FC(48)
+#undef FC
+        default:
+            return launch_smem_class<L>(at, dg, n_half, ci, cap, terms, status, st);
+    }
+}
+
+// Upload the tables and launch every nonempty class (largest classes first).
+int enqueue_fast_classes(const cd* at, const cd* dg, int n_half, const std::vector<Seg>& segs,
+                         int batch, long long term_stride, long long at_stride, long long dg_stride,
+                         int loops, int cap, cd* terms, int8_t* status, void* table_ws,
+                         cudaStream_t st) {
+    const int D = n_half;
+    ClassTables t = build_tables(D, segs);
+    const size_t nseg = segs.size();
+    char* p = static_cast<char*>(table_ws);
+    unsigned long long* d_binom = reinterpret_cast<unsigned long long*>(p);
+    p += align256(sizeof(g_binom_host));
+    Seg* d_segs = reinterpret_cast<Seg*>(p);
+    p += align256(sizeof(Seg) * nseg);
+    long long* d_prefix = reinterpret_cast<long long*>(p);
+    p += align256(sizeof(long long) * t.prefix.size());
+    unsigned long long* d_base = reinterpret_cast<unsigned long long*>(p);
+    CK(cudaMemcpyAsync(d_binom, g_binom_host, sizeof(g_binom_host), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_segs, segs.data(), sizeof(Seg) * nseg, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_prefix, t.prefix.data(), sizeof(long long) * t.prefix.size(),
+                       cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_base, t.base.data(), sizeof(unsigned long long) * t.base.size(),
+                       cudaMemcpyHostToDevice, st));
+    for (int m = D; m >= 1; --m) {
+        long long per = t.count(m);
+        if (per == 0) continue;
+        ClassItems ci;
+        ci.binom = d_binom;
+        ci.segs = d_segs;
+        ci.prefix = d_prefix + (size_t)m * (nseg + 1);
+        ci.base = d_base + (size_t)m * nseg;
+        ci.nseg = (int)nseg;
+        ci.m = m;
+        ci.D = D;
+        ci.per_problem = per;
+        ci.n_items = per * batch;
+        ci.term_stride = term_stride;
+        ci.at_stride = at_stride;
+        ci.dg_stride = dg_stride;
+        cudaError_t e = loops ? launch_fast_class<true>(2 * m, at, dg, n_half, ci, cap, terms, status, st)
+                              : launch_fast_class<false>(2 * m, at, dg, n_half, ci, cap, terms, status, st);
+        ++g_launches;
+        if (e != cudaSuccess) return cuda_fail("fast class launch", e);
+    }
+    return HAFB_OK;
+}
+
+size_t table_ws_bytes(int n_half, size_t nseg) {
+    return align256(sizeof(g_binom_host)) + align256(sizeof(Seg) * nseg) + align256(sizeof(long long) * (n_half + 1) * (nseg + 1)) +
+           align256(sizeof(unsigned long long) * (n_half + 1) * nseg);
+}
+
+size_t mask_range_ws_bytes(int n_half, long long count) {
+    return terms_ws_bytes(count) + table_ws_bytes(n_half, 1);
+}
+
+size_t range_list_ws_bytes(int n_half, int n_ranges, int count) {
+    long long items = (long long)count * (long long)std_width(n_half, n_ranges);
+    return terms_ws_bytes(items) + table_ws_bytes(n_half, count) + align256(sizeof(int32_t) * count);
+}
+
 // enqueue: terms over masks [lo, hi), Kahan per chunk -> partials
 int enqueue_mask_range(const cd* at, const cd* dg, int n_half, uint64_t lo, uint64_t hi,
                        int n_chunks, int backend, int loops, int cap, int arith, void* ws,
                        size_t ws_bytes, cd* partials, long long* fails, cudaStream_t st) {
-    (void)arith;
     long long count = (long long)(hi - lo);
-    if (ws_bytes < terms_ws_bytes(count)) return fail(HAFB_ERR_ARG, "workspace too small");
+    if (ws_bytes < mask_range_ws_bytes(n_half, count)) return fail(HAFB_ERR_ARG, "workspace too small");
     cd* terms;
     int8_t* status;
     carve_terms_ws(ws, count, &terms, &status);
-    if (count > 0)
-        CK(launch_terms(backend, loops, at, dg, n_half, plain_map(lo), count, count, cap, 0, 0,
-                        terms, status, st));
+    if (count > 0) {
+        if (arith == HAFB_ARITH_FAST && backend == 1) {
+            std::vector<Seg> segs(1);
+            segs[0].lo = lo;
+            segs[0].hi = hi;
+            segs[0].out_off = 0;
+            void* tw = static_cast<char*>(ws) + terms_ws_bytes(count);
+            int rc = enqueue_fast_classes(at, dg, n_half, segs, 1, 0, 0, 0, loops, cap, terms,
+                                          status, tw, st);
+            if (rc) return rc;
+        } else {
+            CK(launch_terms(backend, loops, at, dg, n_half, plain_map(lo), count, count, cap, 0, 0,
+                            terms, status, st));
+        }
+    }
     uint64_t width = (hi - lo + n_chunks - 1) / n_chunks;
     int thr = 128;
     range_kahan_kernel<<<(n_chunks + thr - 1) / thr, thr, 0, st>>>(terms, status, lo, hi, width,
@@ -162,29 +347,48 @@ int enqueue_mask_range(const cd* at, const cd* dg, int n_half, uint64_t lo, uint
     return HAFB_OK;
 }
 
-// enqueue: terms over the listed standard ranges, Kahan per range -> partials[i]
-int enqueue_range_list(const cd* at, const cd* dg, int n_half, int n_ranges, const int32_t* d_ranges,
+// enqueue: terms over the listed standard ranges (host list), Kahan per range -> partials[i]
+int enqueue_range_list(const cd* at, const cd* dg, int n_half, int n_ranges, const int32_t* h_ranges,
                        int count, int backend, int loops, int cap, int arith, void* ws,
-                       size_t ws_bytes, cd* partials, long long* fails, cudaStream_t st) {
-    (void)arith;
-    uint64_t width = std_width(n_half, n_ranges);
+                       size_t ws_bytes, cd* partials, long long* fails, cudaStream_t st,
+                       cudaEvent_t terms_done = nullptr) {
+    const uint64_t width = std_width(n_half, n_ranges);
+    const uint64_t total = 1ull << n_half;
     long long items = (long long)count * (long long)width;
-    if (ws_bytes < terms_ws_bytes(items)) return fail(HAFB_ERR_ARG, "workspace too small");
+    if (ws_bytes < range_list_ws_bytes(n_half, n_ranges, count)) return fail(HAFB_ERR_ARG, "workspace too small");
     cd* terms;
     int8_t* status;
     carve_terms_ws(ws, items, &terms, &status);
-    MaskMap map;
-    map.lo = 0;
-    map.mask_list = nullptr;
-    map.range_list = d_ranges;
-    map.width = width;
-    map.total = 1ull << n_half;
-    if (items > 0)
-        CK(launch_terms(backend, loops, at, dg, n_half, map, items, items, cap, 0, 0, terms, status,
-                        st));
+    char* tw = static_cast<char*>(ws) + terms_ws_bytes(items);
+    int32_t* d_ranges = reinterpret_cast<int32_t*>(tw + table_ws_bytes(n_half, count));
+    CK(cudaMemcpyAsync(d_ranges, h_ranges, sizeof(int32_t) * count, cudaMemcpyHostToDevice, st));
+    if (items > 0) {
+        if (arith == HAFB_ARITH_FAST && backend == 1) {
+            std::vector<Seg> segs(count);
+            for (int p = 0; p < count; ++p) {
+                uint64_t a = 1 + (uint64_t)h_ranges[p] * width;
+                segs[p].lo = std::min(a, total);
+                segs[p].hi = std::min(a + width, total);
+                segs[p].out_off = (long long)p * (long long)width;
+            }
+            int rc = enqueue_fast_classes(at, dg, n_half, segs, 1, 0, 0, 0, loops, cap, terms,
+                                          status, tw, st);
+            if (rc) return rc;
+        } else {
+            MaskMap map;
+            map.lo = 0;
+            map.mask_list = nullptr;
+            map.range_list = d_ranges;
+            map.width = width;
+            map.total = total;
+            CK(launch_terms(backend, loops, at, dg, n_half, map, items, items, cap, 0, 0, terms,
+                            status, st));
+        }
+    }
+    if (terms_done) CK(cudaEventRecord(terms_done, st));
     int thr = 128;
     list_kahan_kernel<<<(count + thr - 1) / thr, thr, 0, st>>>(terms, status, d_ranges, count, width,
-                                                               1ull << n_half, partials, fails);
+                                                               total, partials, fails);
     ++g_launches;
     CK(cudaGetLastError());
     return HAFB_OK;
@@ -256,13 +460,13 @@ int64_t hafb_launch_count(int reset) {
 size_t hafb_range_workspace_bytes(int n_half, uint64_t lo, uint64_t hi, int n_chunks) {
     (void)n_half;
     (void)n_chunks;
-    if (hi < lo) return 0;
-    return terms_ws_bytes((long long)(hi - lo));
+    if (hi < lo || n_half < 1 || n_half > kMaxHalf) return 0;
+    return mask_range_ws_bytes(n_half, (long long)(hi - lo));
 }
 
 size_t hafb_range_list_workspace_bytes(int n_half, int n_ranges, int count) {
     if (n_half < 1 || n_half > kMaxHalf || n_ranges < 1 || count < 0) return 0;
-    return terms_ws_bytes((long long)count * (long long)std_width(n_half, n_ranges));
+    return range_list_ws_bytes(n_half, n_ranges, count);
 }
 
 int hafb_sum_mask_range_async(const double* d_atilde, const double* d_diag, int n_half,
@@ -283,21 +487,24 @@ int hafb_sum_mask_range_async(const double* d_atilde, const double* d_diag, int 
 }
 
 int hafb_sum_range_list_async(const double* d_atilde, const double* d_diag, int n_half,
-                              int n_ranges, const int32_t* d_ranges, int count, int backend,
+                              int n_ranges, const int32_t* ranges, int count, int backend,
                               int include_loops, int cap_mult, int arith, void* d_workspace,
                               size_t workspace_bytes, double* d_partials, int64_t* d_fails,
-                              void* stream) {
+                              void* stream, void* terms_done_event) {
     g_err.clear();
     int rc = check_common(n_half, backend, arith);
     if (rc) return rc;
     if (n_ranges < 1 || count < 0) return fail(HAFB_ERR_ARG, "bad range list");
+    for (int i = 0; i < count; ++i)
+        if (ranges[i] < 0 || ranges[i] >= n_ranges) return fail(HAFB_ERR_ARG, "range index out of bounds");
     if (count == 0) return HAFB_OK;
     return enqueue_range_list(reinterpret_cast<const cd*>(d_atilde),
-                              reinterpret_cast<const cd*>(d_diag), n_half, n_ranges, d_ranges, count,
+                              reinterpret_cast<const cd*>(d_diag), n_half, n_ranges, ranges, count,
                               backend, include_loops, cap_mult, arith, d_workspace, workspace_bytes,
                               reinterpret_cast<cd*>(d_partials),
                               reinterpret_cast<long long*>(d_fails),
-                              static_cast<cudaStream_t>(stream));
+                              static_cast<cudaStream_t>(stream),
+                              static_cast<cudaEvent_t>(terms_done_event));
 }
 
 int hafb_sum_mask_range(const double* atilde, const double* diag, int n_half, uint64_t lo,
@@ -308,7 +515,7 @@ int hafb_sum_mask_range(const double* atilde, const double* diag, int n_half, ui
     if (rc) return rc;
     if (hi < lo || hi > (1ull << n_half) || n_chunks < 1) return fail(HAFB_ERR_ARG, "bad mask range");
     const int n = 2 * n_half;
-    size_t ws_bytes = terms_ws_bytes((long long)(hi - lo));
+    size_t ws_bytes = mask_range_ws_bytes(n_half, (long long)(hi - lo));
     Call c;
     cd *d_at, *d_dg, *d_part;
     long long* d_fail;
@@ -341,23 +548,20 @@ int hafb_sum_range_list(const double* atilde, const double* diag, int n_half, in
         if (ranges[i] < 0 || ranges[i] >= n_ranges) return fail(HAFB_ERR_ARG, "range index out of bounds");
     if (count == 0) return HAFB_OK;
     const int n = 2 * n_half;
-    size_t ws_bytes = hafb_range_list_workspace_bytes(n_half, n_ranges, count);
+    size_t ws_bytes = range_list_ws_bytes(n_half, n_ranges, count);
     Call c;
     cd *d_at, *d_dg, *d_part;
     long long* d_fail;
-    int32_t* d_r;
     void* d_ws;
     CK(c.open(device));
     CK(c.alloc(&d_at, sizeof(cd) * n * n));
     CK(c.alloc(&d_dg, sizeof(cd) * n));
-    CK(c.alloc(&d_r, sizeof(int32_t) * count));
     CK(c.alloc(&d_ws, ws_bytes));
     CK(c.alloc(&d_part, sizeof(cd) * count));
     CK(c.alloc(&d_fail, sizeof(long long) * count));
     CK(cudaMemcpyAsync(d_at, atilde, sizeof(cd) * n * n, cudaMemcpyHostToDevice, c.st));
     CK(cudaMemcpyAsync(d_dg, diag, sizeof(cd) * n, cudaMemcpyHostToDevice, c.st));
-    CK(cudaMemcpyAsync(d_r, ranges, sizeof(int32_t) * count, cudaMemcpyHostToDevice, c.st));
-    rc = enqueue_range_list(d_at, d_dg, n_half, n_ranges, d_r, count, backend, include_loops,
+    rc = enqueue_range_list(d_at, d_dg, n_half, n_ranges, ranges, count, backend, include_loops,
                             cap_mult, arith, d_ws, ws_bytes, d_part, d_fail, c.st);
     if (rc) return rc;
     CK(cudaMemcpyAsync(partials, d_part, sizeof(cd) * count, cudaMemcpyDeviceToHost, c.st));
@@ -388,7 +592,7 @@ int hafb_sum_subsets_fast(const double* atilde, const double* diag, int n_half, 
     const uint64_t total = 1ull << n_half;
     const long long count = (long long)(total - 1);
     const uint64_t width = std_width(n_half, n_ranges);
-    size_t ws_bytes = terms_ws_bytes(count);
+    size_t ws_bytes = mask_range_ws_bytes(n_half, count);
     Call c;
     cd *d_at, *d_dg, *d_sum, *terms;
     long long* d_fail;
@@ -403,8 +607,19 @@ int hafb_sum_subsets_fast(const double* atilde, const double* diag, int n_half, 
     CK(cudaMemcpyAsync(d_at, atilde, sizeof(cd) * n * n, cudaMemcpyHostToDevice, c.st));
     CK(cudaMemcpyAsync(d_dg, diag, sizeof(cd) * n, cudaMemcpyHostToDevice, c.st));
     carve_terms_ws(d_ws, count, &terms, &status);
-    CK(launch_terms(backend, include_loops, d_at, d_dg, n_half, plain_map(1), count, count,
-                    cap_mult, 0, 0, terms, status, c.st));
+    if (arith == HAFB_ARITH_FAST && backend == 1) {
+        std::vector<Seg> segs(1);
+        segs[0].lo = 1;
+        segs[0].hi = total;
+        segs[0].out_off = 0;
+        rc = enqueue_fast_classes(d_at, d_dg, n_half, segs, 1, 0, 0, 0, include_loops, cap_mult,
+                                  terms, status, static_cast<char*>(d_ws) + terms_ws_bytes(count),
+                                  c.st);
+        if (rc) return rc;
+    } else {
+        CK(launch_terms(backend, include_loops, d_at, d_dg, n_half, plain_map(1), count, count,
+                        cap_mult, 0, 0, terms, status, c.st));
+    }
     worker_kahan_kernel<<<(workers + 127) / 128, 128, 0, c.st>>>(terms, status, total, width,
                                                                  n_ranges, workers, d_sum, d_fail);
     ++g_launches;
@@ -471,7 +686,9 @@ int hafb_batch(const double* atilde, const double* diag, int batch, int n_half, 
     cd *d_at, *d_dg, *d_t, *d_part, *d_res;
     int8_t* d_s;
     long long* d_fail;
+    void* d_tab;
     CK(c.open(device));
+    CK(c.alloc(&d_tab, table_ws_bytes(n_half, 1)));
     CK(c.alloc(&d_at, sizeof(cd) * n * n * (size_t)batch));
     CK(c.alloc(&d_dg, sizeof(cd) * n * (size_t)batch));
     CK(c.alloc(&d_t, sizeof(cd) * cnt));
@@ -481,8 +698,18 @@ int hafb_batch(const double* atilde, const double* diag, int batch, int n_half, 
     CK(c.alloc(&d_res, sizeof(cd) * batch));
     CK(cudaMemcpyAsync(d_at, atilde, sizeof(cd) * n * n * (size_t)batch, cudaMemcpyHostToDevice, c.st));
     CK(cudaMemcpyAsync(d_dg, diag, sizeof(cd) * n * (size_t)batch, cudaMemcpyHostToDevice, c.st));
-    CK(launch_terms(backend, include_loops, d_at, d_dg, n_half, plain_map(1), per, (long long)cnt,
-                    cap_mult, (long long)n * n, n, d_t, d_s, c.st));
+    if (arith == HAFB_ARITH_FAST && backend == 1) {
+        std::vector<Seg> segs(1);
+        segs[0].lo = 1;
+        segs[0].hi = total;
+        segs[0].out_off = 0;
+        rc = enqueue_fast_classes(d_at, d_dg, n_half, segs, batch, per, (long long)n * n, n,
+                                  include_loops, cap_mult, d_t, d_s, d_tab, c.st);
+        if (rc) return rc;
+    } else {
+        CK(launch_terms(backend, include_loops, d_at, d_dg, n_half, plain_map(1), per,
+                        (long long)cnt, cap_mult, (long long)n * n, n, d_t, d_s, c.st));
+    }
     // problem b's term for mask q+1 sits at b*per + q: the reduce runs with lo = 1
     {
         int thr = 128;
@@ -558,3 +785,44 @@ int hafb_charpoly_coefficients(const double* b, int m, int arith, int device, do
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ calibration
+namespace {
+// 8 independent DFMA chains per thread: the FP64 pipe's issue-limited peak.
+__global__ void __launch_bounds__(256) dfma_probe_kernel(double* out, int iters, double a, double b) {
+    double x0 = threadIdx.x * 1e-9, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5,
+           x6 = x0 + 6, x7 = x0 + 7;
+    for (int i = 0; i < iters; ++i) {
+        x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+        x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+    double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+    if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+}  // namespace
+
+extern "C" int hafb_fp64_peak(int device, double* tflops, double* ms) {
+    g_err.clear();
+    Call c;
+    double* d_out;
+    CK(c.open(device));
+    CK(c.alloc(&d_out, sizeof(double)));
+    int sms = sm_count();
+    const int blocks = sms * 8, threads = 256, iters = 1 << 16;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    dfma_probe_kernel<<<blocks, threads, 0, c.st>>>(d_out, 1024, 0.999999, 1e-7);  // warm-up
+    CK(cudaEventRecord(e0, c.st));
+    dfma_probe_kernel<<<blocks, threads, 0, c.st>>>(d_out, iters, 0.999999, 1e-7);
+    CK(cudaEventRecord(e1, c.st));
+    CK(cudaEventSynchronize(e1));
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const double flop = 2.0 * 8.0 * (double)iters * blocks * threads;
+    *ms = t;
+    *tflops = flop / (t * 1e-3) / 1e12;
+    return HAFB_OK;
+}

@@ -1,0 +1,525 @@
+// term_fast.cuh -- register-resident FAST subset-term kernel (charpoly backend).
+//
+// One TEAM of W lanes evaluates one pair subset of size S = 2m (W = S rounded
+// up to a power of two, 2..64; W = 64 spans two warps).  Lane r of the team
+// owns row r of the subset matrix B = X.A_Z in registers, so the two O(S^3)
+// parts of the Hessenberg reduction (_numba.py:36-67) are lane-local:
+//   rank-1 row update  h[i,k] -= mu_i h[p,k]     (pivot row broadcast from smem)
+//   column gemv        h[k,p] += sum_i mu_i h[k,i] (mu broadcast from smem)
+// and they are fused into one pass over the columns with FMA-contracted
+// complex multiply-adds.  Exact-arithmetic identities used (results agree with
+// the reference to rounding, not bit for bit -- MIRROR mode is term_smem.cuh):
+//   * L^{-1} H L is applied as (L^{-1} H) L instead of interleaving each i;
+//   * pivot choice by |re|+|im| (the reference uses hypot);
+//   * the row swap of the pivoting is a relabelling of which lane holds which
+//     logical row (no data movement); the column swap is a register swap;
+//   * Newton's identities and the exp-series coefficient use the O(D^2)
+//     recurrences (e' = s' e), parallel over the coefficient index;
+//   * the charpoly leading-minor recurrence (_numba.py:203-225) is evaluated
+//     with lane d owning coefficient d of every P_k.
+// Columns retire into shared memory as the reduction advances (column j is
+// final after step j), so the register window shifts left every two steps and
+// the step body has static register indices without unrolling over j.
+#pragma once
+
+#include <type_traits>
+
+#include "cplx.cuh"
+#include "enumerate.cuh"
+
+namespace hafb {
+
+// Compile-time loop: f(std::integral_constant<int, I>) for I = B, B+STEP, ... < E,
+// stopping early when f returns false.  Guarantees static register indices
+// (a #pragma unroll loop with an early exit is not always fully unrolled, and a
+// partially unrolled register array is demoted to local memory).
+template <int I>
+using ic = std::integral_constant<int, I>;
+
+template <int B, int E, int STEP = 1, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+    if constexpr (B < E) {
+        if (f(ic<B>{})) static_for<B + STEP, E, STEP>(f);
+    }
+}
+
+template <int S>
+struct TeamWidth {
+    static constexpr int W = S <= 2 ? 2 : S <= 4 ? 4 : S <= 8 ? 8 : S <= 16 ? 16 : S <= 32 ? 32 : 64;
+};
+
+constexpr int kFastThreads = 128;
+constexpr int kDMax = 31;
+
+// packed upper-Hessenberg storage, column-major: column c holds rows 0..min(c+1, S-1)
+// and starts at c(c+3)/2.
+__host__ __device__ constexpr int hs_elems(int S) { return (S - 1) * (S + 2) / 2 + S; }
+
+template <int S>
+struct FastLayout {
+    static constexpr int HS = 0;
+    static constexpr int SP = S + 4;                  // padded pivot-row / multiplier length
+    static constexpr int PR = HS + hs_elems(S);       // [2][SP] pivot rows
+    static constexpr int MU = PR + 2 * SP;            // [2][SP] multipliers
+    static constexpr int CF = MU + 2 * SP;            // [2][S] charpoly coefs
+    static constexpr int RED = CF + 2 * S;            // [2][2][2] argmax exchange (W = 64)
+    static constexpr int A = RED + 8;                 // [S+1] charpoly coefficients
+    static constexpr int U = A + S + 1;               // [2][S] loop-chain vector
+    static constexpr int PX = U + 2 * S;              // [S] charpoly cross-warp exchange
+    static constexpr int T = PX + S;                  // [kDMax+2] traces / exp broadcast
+    static constexpr int G = T + kDMax + 2;           // [kDMax+2] g_j = j s_j
+    static constexpr int FLAG = G + kDMax + 2;        // [1]
+    static constexpr int SIGN = (S + 3) / 4 + 1;      // cd slots holding S ints
+    static constexpr int SIG = FLAG + 2;              // [2][S] int column permutation
+    static constexpr int TOTAL = SIG + 2 * SIGN;
+};
+
+template <int W>
+struct TeamCtx {
+    int lane;  // rank within the team
+    int tib;   // team index within the block
+    unsigned wmask;
+    __device__ __forceinline__ void sync() const {
+        if constexpr (W <= 32) {
+            __syncwarp(wmask);
+        } else {
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + tib), "r"(W) : "memory");
+        }
+    }
+};
+
+template <int W>
+__device__ __forceinline__ bool lane_is(const TeamCtx<W>& tc, int r) {
+    return tc.lane == r;
+}
+
+template <int W>
+__device__ __forceinline__ double tshfl_xor(double v, int off) {
+    return __shfl_xor_sync(0xffffffffu, v, off, W < 32 ? W : 32);
+}
+template <int W>
+__device__ __forceinline__ int tshfl_xor(int v, int off) {
+    return __shfl_xor_sync(0xffffffffu, v, off, W < 32 ? W : 32);
+}
+template <int W>
+__device__ __forceinline__ double tshfl(double v, int src) {
+    return __shfl_sync(0xffffffffu, v, src, W < 32 ? W : 32);
+}
+template <int W>
+__device__ __forceinline__ double tshfl_up(double v, int d) {
+    return __shfl_up_sync(0xffffffffu, v, d, W < 32 ? W : 32);
+}
+
+__device__ __forceinline__ cd f_add(cd a, cd b) { return mk(a.re + b.re, a.im + b.im); }
+__device__ __forceinline__ cd f_inv(cd p) {
+    double r = 1.0 / fma(p.re, p.re, p.im * p.im);
+    return mk(p.re * r, -p.im * r);
+}
+
+// team argmax over (key, row): larger key wins, ties -> smaller row; returns the
+// winner's key, row and its column-j value p.
+template <int W>
+__device__ __forceinline__ void team_argmax(const TeamCtx<W>& tc, cd* red, double& key, int& row,
+                                            cd& pv) {
+    constexpr int WW = W < 32 ? W : 32;
+#pragma unroll
+    for (int off = WW / 2; off > 0; off >>= 1) {
+        double ok = tshfl_xor<W>(key, off);
+        int orow = tshfl_xor<W>(row, off);
+        double opr = tshfl_xor<W>(pv.re, off);
+        double opi = tshfl_xor<W>(pv.im, off);
+        if (ok > key || (ok == key && orow < row)) {
+            key = ok;
+            row = orow;
+            pv = mk(opr, opi);
+        }
+    }
+    if constexpr (W > 32) {
+        const int w = tc.lane >> 5;
+        if ((tc.lane & 31) == 0) {
+            red[2 * w] = mk(key, (double)row);
+            red[2 * w + 1] = pv;
+        }
+        tc.sync();
+        cd a0 = red[0], p0 = red[1], a1 = red[2], p1 = red[3];
+        if (a1.re > a0.re || (a1.re == a0.re && a1.im < a0.im)) {
+            a0 = a1;
+            p0 = p1;
+        }
+        key = a0.re;
+        row = (int)a0.im;
+        pv = p0;
+    }
+}
+
+// Register moves that the compiler may not if-convert into selects: with them the
+// column swap below stays a short uniform branch tree (~5 compares + 8 moves)
+// instead of an 8-FSEL-per-candidate select chain.
+__device__ __forceinline__ void vmov(double& d, double s) {
+    asm volatile("mov.b64 %0, %1;" : "=d"(d) : "d"(s));
+}
+
+// swap hr[A] <-> hr[b] for a team-uniform runtime b in [LO, HI) (binary branch tree)
+template <int S, int LO, int HI>
+__device__ __forceinline__ void swap_bs(cd (&hr)[S], int A, int b) {
+    if constexpr (HI - LO == 1) {
+        const cd t = hr[A];
+        vmov(hr[A].re, hr[LO].re);
+        vmov(hr[A].im, hr[LO].im);
+        vmov(hr[LO].re, t.re);
+        vmov(hr[LO].im, t.im);
+    } else if constexpr (HI > LO) {
+        constexpr int MID = (LO + HI) / 2;
+        if (b < MID) swap_bs<S, LO, MID>(hr, A, b);
+        else swap_bs<S, MID, HI>(hr, A, b);
+    }
+}
+
+// Team argmax of a nonnegative pivot key: the key is rounded to float, its low 6
+// mantissa bits replaced by (63 - lane) and the packed words max-reduced with one
+// redux.sync per warp.  Returns the winning lane (ties -> lowest lane) and the
+// winning float key bits (0 if every key is 0).
+template <int W>
+__device__ __forceinline__ int team_argmax_lane(const TeamCtx<W>& tc, cd* red, double key,
+                                                unsigned& kbits) {
+    const unsigned kb = key > 0.0 ? __float_as_uint(__double2float_ru(key)) : 0u;
+    unsigned packed = (kb & ~63u) | (unsigned)(63 - tc.lane);
+    unsigned mx;
+    if constexpr (W <= 32) {
+        mx = __reduce_max_sync(tc.wmask, packed);
+    } else {
+        mx = __reduce_max_sync(0xffffffffu, packed);
+        unsigned* r = reinterpret_cast<unsigned*>(red);
+        if ((tc.lane & 31) == 0) r[tc.lane >> 5] = mx;
+        tc.sync();
+        const unsigned a0 = r[0], a1 = r[1];
+        mx = a0 > a1 ? a0 : a1;
+    }
+    kbits = mx & ~63u;
+    return 63 - (int)(mx & 63u);
+}
+
+// Hessenberg step J (static): column J is hr[J]; columns < J are retired to smem.
+// Pivoting relabels rows (lane <-> logical row `myrow`, no data movement) and
+// swaps register columns J+1 <-> brow with a uniform branch tree.
+template <int S, int W, int J>
+__device__ __forceinline__ void fast_hess_step(cd (&hr)[S], int& myrow, const TeamCtx<W>& tc,
+                                               cd* ws) {
+    using L = FastLayout<S>;
+    constexpr int B = J & 1;  // double buffer of the broadcasts
+    const cd hj = hr[J];
+    const double key = (myrow > J && myrow < S) ? fabs(hj.re) + fabs(hj.im) : 0.0;
+    unsigned kbits;
+    const int wl = team_argmax_lane<W>(tc, ws + L::RED + 4 * B, key, kbits);
+    cd* Hs = ws + L::HS;
+    constexpr int CS = (J * (J + 3)) / 2;  // start of column J in the packed store
+    if (kbits == 0u) {  // nothing to eliminate below the subdiagonal
+        if (myrow <= J + 1) Hs[CS + myrow] = hj;
+        return;
+    }
+    int brow;
+    cd p;
+    if constexpr (W <= 32) {
+        const int src = ((int)(threadIdx.x & 31) & ~(W - 1)) + wl;  // warp lane of the winner
+        brow = __shfl_sync(tc.wmask, myrow, src);
+        p.re = __shfl_sync(tc.wmask, hj.re, src);
+        p.im = __shfl_sync(tc.wmask, hj.im, src);
+    } else {
+        cd* r = ws + L::RED + 4 * B + 2;
+        if (tc.lane == wl) {
+            r[0] = hj;
+            r[1] = mk((double)myrow, 0.0);
+        }
+        tc.sync();
+        p = r[0];
+        brow = (int)r[1].re;
+    }
+    if (myrow == brow) myrow = J + 1;
+    else if (myrow == J + 1) myrow = brow;
+    if (myrow <= J + 1) Hs[CS + myrow] = hj;
+    if (brow != J + 1) swap_bs<S, J + 2, S>(hr, J + 1, brow);
+    const cd ip = f_inv(p);
+    const bool elim = myrow >= J + 2 && myrow < S;
+    const cd mu = elim ? f_mul(hj, ip) : mk(0.0, 0.0);
+    cd* pr = ws + L::PR + B * L::SP;
+    cd* mus = ws + L::MU + B * L::SP;
+    if (myrow == J + 1) {
+        static_for<J + 1, S>([&](auto c) {
+            pr[c()] = hr[c()];
+            return true;
+        });
+    }
+    if (elim) mus[myrow] = mu;
+    tc.sync();
+    cd hj1 = f_cms(hr[J + 1], mu, pr[J + 1]);
+    cd acc0 = mk(0.0, 0.0), acc1 = mk(0.0, 0.0);
+    static_for<J + 2, S>([&](auto cc) {
+        constexpr int c = decltype(cc)::value;
+        const cd pv = pr[c], mc = mus[c];
+        hr[c] = f_cms(hr[c], mu, pv);
+        if constexpr (c & 1) acc1 = f_cma(acc1, mc, hr[c]);
+        else acc0 = f_cma(acc0, mc, hr[c]);
+        return true;
+    });
+    hr[J + 1] = f_add(hj1, f_add(acc0, acc1));
+}
+
+template <int S, bool LOOPS>
+__global__ void __launch_bounds__(kFastThreads) fast_term_kernel(const cd* __restrict__ atilde,
+                                                                 const cd* __restrict__ diag,
+                                                                 int n_half, ClassItems ci,
+                                                                 cd* __restrict__ terms,
+                                                                 int8_t* __restrict__ status) {
+    constexpr int W = TeamWidth<S>::W;
+    constexpr int TPB = kFastThreads / W;
+    constexpr int M = S / 2;
+    constexpr int R = (kDMax + W - 1) / W;  // coefficient chunks per lane
+    using L = FastLayout<S>;
+    extern __shared__ cd smem[];
+    TeamCtx<W> tc;
+    tc.tib = threadIdx.x / W;
+    tc.lane = threadIdx.x % W;
+    if constexpr (W < 32) {
+        tc.wmask = ((1u << W) - 1u) << ((threadIdx.x & 31) & ~(W - 1));
+    } else {
+        tc.wmask = 0xffffffffu;
+    }
+    const int lane = tc.lane;
+    cd* ws = smem + (size_t)tc.tib * L::TOTAL;
+    const int opaque_zero = ci.nseg < 0 ? 1 : 0;  // 0, but unknown to the compiler
+    // reciprocals 1/k for the exp recurrence (block-shared, written once)
+    double* INV = reinterpret_cast<double*>(smem + (size_t)TPB * L::TOTAL);
+    for (int k = threadIdx.x; k <= kDMax; k += blockDim.x) INV[k] = k ? 1.0 / k : 0.0;
+    __syncthreads();
+    const int n = 2 * n_half;
+    const int D = n_half;
+    const long long stride = (long long)gridDim.x * TPB;
+
+    for (long long base = (long long)blockIdx.x * TPB; base < ci.n_items; base += stride) {
+        const long long item = base + tc.tib;
+        const bool valid = item < ci.n_items;
+        const ItemRef ir = resolve_item(ci, valid ? item : base);
+        const cd* at = atilde + ir.problem * ci.at_stride;
+        const cd* dg = diag + ir.problem * ci.dg_stride;
+        // vertex list: vertex c = 2*bit[c/2] + (c&1); every index below is static except
+        // the lane's own pair, found with __fns (no dynamically indexed local arrays)
+        int vbit[M];
+        {
+            uint32_t mm = ir.mask;
+#pragma unroll
+            for (int q = 0; q < M; ++q) {
+                vbit[q] = __ffs(mm) - 1;
+                mm &= mm - 1;
+            }
+        }
+        const int mybit = lane < S ? (int)__fns(ir.mask, 0, (lane >> 1) + 1) : 0;
+        cd hr[S];
+        cd* G = ws + L::G;
+        // ---------------------------------------------- loop chain (_numba.py:253-273)
+        if constexpr (LOOPS) {
+            // lane j holds column j of B: B[i][j] = Atilde[v_{j^1}][v_{i^1}]
+            const int rj = 2 * mybit + ((lane & 1) ^ 1);
+            static_for<0, S>([&](auto i) {
+                const int ci1 = 2 * vbit[i() >> 1] + ((i() & 1) ^ 1);
+                hr[i()] = lane < S ? at[rj * n + ci1] : mk(0.0, 0.0);
+                return true;
+            });
+            cd u = lane < S ? dg[2 * mybit + (lane & 1)] : mk(0.0, 0.0);
+            const cd xv = lane < S ? dg[2 * mybit + ((lane & 1) ^ 1)] : mk(0.0, 0.0);
+            cd* U = ws + L::U;
+            for (int k = 1; k <= D; ++k) {
+                cd l = f_mul(u, xv);
+                constexpr int WW = W < 32 ? W : 32;
+#pragma unroll
+                for (int off = WW / 2; off > 0; off >>= 1) {
+                    l.re += tshfl_xor<W>(l.re, off);
+                    l.im += tshfl_xor<W>(l.im, off);
+                }
+                if constexpr (W > 32) {
+                    // combine the two warps' partial sums
+                    cd* X = ws + L::PX;
+                    if ((lane & 31) == 0) X[(k & 1) * 2 + (lane >> 5)] = l;
+                    tc.sync();
+                    l = f_add(X[(k & 1) * 2], X[(k & 1) * 2 + 1]);
+                }
+                if (lane == 0) G[k] = l;  // ell_k; folded into g below
+                if (k < D) {
+                    cd* ub = U + (k & 1) * S;
+                    if (lane < S) ub[lane] = u;
+                    tc.sync();
+                    cd acc0 = mk(0.0, 0.0), acc1 = mk(0.0, 0.0);
+                    static_for<0, S>([&](auto i) {
+                        if constexpr (decltype(i)::value & 1) acc1 = f_cma(acc1, ub[i()], hr[i()]);
+                        else acc0 = f_cma(acc0, ub[i()], hr[i()]);
+                        return true;
+                    });
+                    u = lane < S ? f_add(acc0, acc1) : mk(0.0, 0.0);
+                }
+            }
+        }
+        // ---------------------------------------------- gather B rows
+        const int vr = 2 * mybit + (lane & 1);
+        static_for<0, S>([&](auto c) {
+            const int vc = 2 * vbit[c() >> 1] + (c() & 1);
+            hr[c()] = lane < S ? at[vr * n + vc] : mk(0.0, 0.0);
+            return true;
+        });
+        int myrow = lane;
+        // ---------------------------------------------- Hessenberg (_numba.py:36-67)
+        static_for<0, S - 2>([&](auto jj) {
+            fast_hess_step<S, W, decltype(jj)::value>(hr, myrow, tc, ws);
+            return true;
+        });
+        {
+            cd* Hs = ws + L::HS;
+            if (myrow < S) {
+                Hs[((S - 2) * (S + 1)) / 2 + myrow] = hr[S - 2];
+                Hs[((S - 1) * (S + 2)) / 2 + myrow] = hr[S - 1];
+            }
+        }
+        tc.sync();
+        // ---------------------------------------------- charpoly (_numba.py:203-225)
+        {
+            const cd* Hs = ws + L::HS;
+            cd* A = ws + L::A;
+            cd P[S];
+            P[0] = mk(lane == 0 ? 1.0 : 0.0, 0.0);
+            cd prodl = mk(1.0, 0.0);
+            static_for<1, S + 1>([&](auto kk) {
+                constexpr int k = decltype(kk)::value;
+                cd* cf = ws + L::CF + (k & 1) * S;
+                if constexpr (k >= 2) {
+                    const cd beta = Hs[((k - 2) * (k + 1)) / 2 + (k - 1)];  // h[k-1][k-2]
+                    if (lane <= k - 2) {
+                        prodl = f_mul(lane == k - 2 ? mk(1.0, 0.0) : prodl, beta);
+                        cf[lane] = f_mul(Hs[((k - 1) * (k + 2)) / 2 + lane], prodl);
+                    }
+                }
+                cd prev;
+                if constexpr (W <= 32) {
+                    prev.re = tshfl_up<W>(P[k - 1].re, 1);
+                    prev.im = tshfl_up<W>(P[k - 1].im, 1);
+                } else {
+                    cd* X = ws + L::PX;
+                    if (lane < S) X[lane] = P[k - 1];
+                    tc.sync();
+                    prev = lane >= 1 && lane <= S ? X[lane - 1] : mk(0.0, 0.0);
+                }
+                if (lane == 0) prev = mk(0.0, 0.0);
+                tc.sync();
+                const cd hk = Hs[((k - 1) * (k + 2)) / 2 + (k - 1)];
+                cd acc = f_cms(prev, hk, P[k - 1]);
+                cd acc2 = mk(0.0, 0.0);
+                // chunks of four coefficients; the opaque branch is a basic-block fence
+                // that bounds how many broadcast loads the scheduler hoists at once
+                static_for<1, k, 4>([&](auto ii) {
+                    constexpr int i0 = decltype(ii)::value;
+                    if (i0 >= k + opaque_zero) return false;
+                    static_for<i0, (i0 + 4 < k ? i0 + 4 : k)>([&](auto jj) {
+                        constexpr int i = decltype(jj)::value;
+                        if constexpr (i & 1) acc = f_cms(acc, cf[i - 1], P[i - 1]);
+                        else acc2 = f_cms(acc2, cf[i - 1], P[i - 1]);
+                        return true;
+                    });
+                    return true;
+                });
+                acc = f_add(acc, acc2);
+                if constexpr (k < S) P[k] = acc;
+                else if (lane < S) A[lane] = acc;
+                return true;
+            });
+            if (lane == 0) A[S] = mk(1.0, 0.0);
+            tc.sync();
+        }
+        // ---------------------------------------------- Newton + Cayley-Hamilton (_numba.py:228-250)
+        cd* T = ws + L::T;
+        cd* A = ws + L::A;
+        int bad = 0;
+        {
+            cd acck[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int k = lane + 1 + W * r;
+                acck[r] = (k <= D && k <= S) ? mk(-(double)k * A[S - k].re, -(double)k * A[S - k].im)
+                                             : mk(0.0, 0.0);
+            }
+            for (int kk = 1; kk <= D; ++kk) {
+                const int owner = (kk - 1) % W, chunk = (kk - 1) / W;
+                if (lane == owner) {
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        if (r == chunk) T[kk] = acck[r];
+                }
+                tc.sync();
+                const cd tk = T[kk];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int k = lane + 1 + W * r;
+                    const int jj = k - kk;
+                    if (k <= D && jj >= 1 && jj <= S) acck[r] = f_cms(acck[r], A[S - jj], tk);
+                }
+            }
+            tc.sync();
+            // g_k = k s_k = t_k / 2 (+ k ell_k / 2 with loops)
+            for (int k = lane + 1; k <= D; k += W) {
+                cd tk = T[k];
+                if (!isfinite(tk.re) || !isfinite(tk.im)) bad = 1;
+                cd g = mk(0.5 * tk.re, 0.5 * tk.im);
+                if constexpr (LOOPS) g = mk(fma(0.5 * k, G[k].re, g.re), fma(0.5 * k, G[k].im, g.im));
+                G[k] = g;
+            }
+        }
+        // any lane saw a non-finite trace -> status 2
+        if constexpr (W <= 32) {
+            bad = __any_sync(tc.wmask, bad);
+        } else {
+            if (lane == 0) ws[L::FLAG].re = 0.0;
+            tc.sync();
+            if (bad) ws[L::FLAG].re = 1.0;
+            tc.sync();
+            bad = ws[L::FLAG].re != 0.0;
+        }
+        tc.sync();
+        // ---------------------------------------------- exp coefficient: e_k = (1/k) sum_j g_j e_{k-j}
+        cd eD = mk(0.0, 0.0);
+        {
+            cd acck[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) acck[r] = mk(0.0, 0.0);
+            for (int kk = 0; kk < D; ++kk) {
+                const int owner = (kk - 1 + W) % W, chunk = (kk - 1) / W;
+                if (kk == 0) {
+                    if (lane == 0) T[0] = mk(1.0, 0.0);
+                } else if (lane == owner) {
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        if (r == chunk) {
+                            const double inv = INV[kk];
+                            T[kk] = mk(acck[r].re * inv, acck[r].im * inv);
+                        }
+                }
+                tc.sync();
+                const cd ek = T[kk];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int k = lane + 1 + W * r;
+                    if (k <= D && k > kk) acck[r] = f_cma(acck[r], G[k - kk], ek);
+                }
+            }
+            const int owner = (D - 1) % W, chunk = (D - 1) / W;
+            if (lane == owner) {
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+                    if (r == chunk) eD = mk(acck[r].re * INV[D], acck[r].im * INV[D]);
+            }
+        }
+        if (valid && lane == ((D - 1) % W)) {
+            const bool neg = ((D - M) & 1) != 0;
+            terms[ir.out] = bad ? mk(0.0, 0.0) : (neg ? mk(-eD.re, -eD.im) : eD);
+            status[ir.out] = bad ? 2 : 0;
+        }
+        tc.sync();
+    }
+}
+
+}  // namespace hafb

@@ -19,6 +19,7 @@
 #pragma once
 
 #include "cplx.cuh"
+#include "enumerate.cuh"
 
 namespace hafb {
 
@@ -466,4 +467,33 @@ __global__ void __launch_bounds__(256) terms_smem_kernel(
     }
 }
 
+}  // namespace hafb
+
+namespace hafb {
+// Class-enumerated variant (one popcount class per launch, see enumerate.cuh);
+// used for the sizes the register kernels do not cover.
+template <int BACKEND, bool LOOPS>
+__global__ void __launch_bounds__(256) terms_smem_class_kernel(
+    const cd* __restrict__ atilde, const cd* __restrict__ diag, int n_half, ClassItems ci,
+    int cap_mult, cd* __restrict__ terms, int8_t* __restrict__ status) {
+    extern __shared__ cd smem[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    const int n = 2 * n_half;
+    WarpWs w = carve(smem + (size_t)wib * smem_warp_elems(n), n);
+    const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long it = (long long)blockIdx.x * (blockDim.x >> 5) + wib; it < ci.n_items; it += nwarps) {
+        const ItemRef ir = resolve_item(ci, it);
+        cd t = mk(0.0, 0.0);
+        int st = 0;
+        subset_term_smem<BACKEND, LOOPS>(atilde + ir.problem * ci.at_stride,
+                                         diag + ir.problem * ci.dg_stride, n_half, ir.mask,
+                                         cap_mult, w, lane, t, st);
+        if (lane == 0) {
+            terms[ir.out] = t;
+            status[ir.out] = (int8_t)st;
+        }
+        __syncwarp();
+    }
+}
 }  // namespace hafb

@@ -253,6 +253,8 @@ def run_ours(args):
     lib.hafb_launch_count(1)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
             torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for _, et, _ in evs:  # materialise the lazily created events before the ABI records them
+        et.record(stream)
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()

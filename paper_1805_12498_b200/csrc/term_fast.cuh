@@ -49,6 +49,7 @@ struct TeamWidth {
 };
 
 constexpr int kFastThreads = 128;
+constexpr int kGroup = 2;  // columns per uniform branch in the Hessenberg sweep
 constexpr int kDMax = 31;
 
 // packed upper-Hessenberg storage, column-major: column c holds rows 0..min(c+1, S-1)
@@ -58,7 +59,7 @@ __host__ __device__ constexpr int hs_elems(int S) { return (S - 1) * (S + 2) / 2
 template <int S>
 struct FastLayout {
     static constexpr int HS = 0;
-    static constexpr int SP = S + 4;                  // padded pivot-row / multiplier length
+    static constexpr int SP = S + 8;                  // padded pivot-row / multiplier length
     static constexpr int PR = HS + hs_elems(S);       // [2][SP] pivot rows
     static constexpr int MU = PR + 2 * SP;            // [2][SP] multipliers
     static constexpr int CF = MU + 2 * SP;            // [2][S] charpoly coefs
@@ -199,69 +200,109 @@ __device__ __forceinline__ int team_argmax_lane(const TeamCtx<W>& tc, cd* red, d
     return 63 - (int)(mx & 63u);
 }
 
-// Hessenberg step J (static): column J is hr[J]; columns < J are retired to smem.
-// Pivoting relabels rows (lane <-> logical row `myrow`, no data movement) and
-// swaps register columns J+1 <-> brow with a uniform branch tree.
-template <int S, int W, int J>
-__device__ __forceinline__ void fast_hess_step(cd (&hr)[S], int& myrow, const TeamCtx<W>& tc,
-                                               cd* ws) {
+// Hessenberg reduction (_numba.py:36-67) as a ROLLED loop over steps on a shifting
+// register window: at step J, w[c] holds logical column J + c of the lane's row
+// (c < S - J live positions).  The pivot column is always w[0] and the column-op
+// target always w[1]; the trailing columns are processed in pairs under a
+// warp-uniform guard (c < live), and the window shifts left by one per step, so
+// every register index is static while the code stays one step body long
+// (a fully unrolled reduction is ~20K instructions and misses in the i-cache).
+// Rows are relabelled (lane <-> logical row `myrow`); the pivot column swap is a
+// uniform branch tree over the window.
+template <int S, int W>
+__device__ __forceinline__ void fast_hessenberg(cd (&w)[S], int& myrow, const TeamCtx<W>& tc,
+                                                cd* ws) {
     using L = FastLayout<S>;
-    constexpr int B = J & 1;  // double buffer of the broadcasts
-    const cd hj = hr[J];
-    const double key = (myrow > J && myrow < S) ? fabs(hj.re) + fabs(hj.im) : 0.0;
-    unsigned kbits;
-    const int wl = team_argmax_lane<W>(tc, ws + L::RED + 4 * B, key, kbits);
     cd* Hs = ws + L::HS;
-    constexpr int CS = (J * (J + 3)) / 2;  // start of column J in the packed store
-    if (kbits == 0u) {  // nothing to eliminate below the subdiagonal
-        if (myrow <= J + 1) Hs[CS + myrow] = hj;
-        return;
-    }
-    int brow;
-    cd p;
-    if constexpr (W <= 32) {
-        const int src = ((int)(threadIdx.x & 31) & ~(W - 1)) + wl;  // warp lane of the winner
-        brow = __shfl_sync(tc.wmask, myrow, src);
-        p.re = __shfl_sync(tc.wmask, hj.re, src);
-        p.im = __shfl_sync(tc.wmask, hj.im, src);
-    } else {
-        cd* r = ws + L::RED + 4 * B + 2;
-        if (tc.lane == wl) {
-            r[0] = hj;
-            r[1] = mk((double)myrow, 0.0);
+#pragma unroll 1
+    for (int J = 0; J < S - 2; ++J) {
+        const int live = S - J;
+        const int B = J & 1;  // double buffers of the broadcasts
+        const cd hj = w[0];
+        const double key = (myrow > J && myrow < S) ? fabs(hj.re) + fabs(hj.im) : 0.0;
+        unsigned kbits;
+        const int wl = team_argmax_lane<W>(tc, ws + L::RED + 4 * B, key, kbits);
+        const int CS = (J * (J + 3)) / 2;  // start of column J in the packed store
+        if (kbits != 0u) {
+            int brow;
+            cd p;
+            if constexpr (W <= 32) {
+                const int src = ((int)(threadIdx.x & 31) & ~(W - 1)) + wl;
+                brow = __shfl_sync(tc.wmask, myrow, src);
+                p.re = __shfl_sync(tc.wmask, hj.re, src);
+                p.im = __shfl_sync(tc.wmask, hj.im, src);
+            } else {
+                cd* r = ws + L::RED + 4 * B + 2;
+                if (tc.lane == wl) {
+                    r[0] = hj;
+                    r[1] = mk((double)myrow, 0.0);
+                }
+                tc.sync();
+                p = r[0];
+                brow = (int)r[1].re;
+            }
+            if (myrow == brow) myrow = J + 1;
+            else if (myrow == J + 1) myrow = brow;
+            if (myrow <= J + 1) Hs[CS + myrow] = hj;
+            if (brow != J + 1) swap_bs<S, 2, S>(w, 1, brow - J);
+            const cd ip = f_inv(p);
+            const bool elim = myrow >= J + 2 && myrow < S;
+            const cd mu = elim ? f_mul(hj, ip) : mk(0.0, 0.0);
+            cd* pr = ws + L::PR + B * L::SP;
+            cd* mus = ws + L::MU + B * L::SP;
+            if (myrow == J + 1) {
+                pr[1] = w[1];
+                static_for<2, S, kGroup>([&](auto gg) {
+                    constexpr int c0 = decltype(gg)::value;
+                    if (c0 < live) {
+                        static_for<c0, (c0 + kGroup < S ? c0 + kGroup : S)>([&](auto c) {
+                            pr[c()] = w[c()];
+                            return true;
+                        });
+                    }
+                    return true;
+                });
+                // zero padding: the last group may run past the live edge
+#pragma unroll
+                for (int z = 0; z < kGroup; ++z) {
+                    pr[live + z] = mk(0.0, 0.0);
+                    mus[live + z] = mk(0.0, 0.0);
+                }
+            }
+            if (elim) mus[myrow - J] = mu;
+            tc.sync();
+            const cd hj1 = f_cms(w[1], mu, pr[1]);
+            cd acc0 = mk(0.0, 0.0), acc1 = mk(0.0, 0.0);
+            // columns in groups of kGroup under one uniform branch
+            static_for<2, S, kGroup>([&](auto gg) {
+                constexpr int c0 = decltype(gg)::value;
+                if (c0 < live) {
+                    static_for<c0, (c0 + kGroup < S ? c0 + kGroup : S)>([&](auto cc) {
+                        constexpr int c = decltype(cc)::value;
+                        const cd pv = pr[c], mc = mus[c];
+                        w[c] = f_cms(w[c], mu, pv);
+                        if constexpr (c & 1) acc1 = f_cma(acc1, mc, w[c]);
+                        else acc0 = f_cma(acc0, mc, w[c]);
+                        return true;
+                    });
+                }
+                return true;
+            });
+            w[1] = f_add(hj1, f_add(acc0, acc1));
+        } else {  // nothing to eliminate below the subdiagonal
+            if (myrow <= J + 1) Hs[CS + myrow] = hj;
         }
-        tc.sync();
-        p = r[0];
-        brow = (int)r[1].re;
-    }
-    if (myrow == brow) myrow = J + 1;
-    else if (myrow == J + 1) myrow = brow;
-    if (myrow <= J + 1) Hs[CS + myrow] = hj;
-    if (brow != J + 1) swap_bs<S, J + 2, S>(hr, J + 1, brow);
-    const cd ip = f_inv(p);
-    const bool elim = myrow >= J + 2 && myrow < S;
-    const cd mu = elim ? f_mul(hj, ip) : mk(0.0, 0.0);
-    cd* pr = ws + L::PR + B * L::SP;
-    cd* mus = ws + L::MU + B * L::SP;
-    if (myrow == J + 1) {
-        static_for<J + 1, S>([&](auto c) {
-            pr[c()] = hr[c()];
+        // (per-position predicated moves: this form keeps register pressure lowest)
+        static_for<0, S - 1>([&](auto c) {
+            if (c() + 1 < live) w[c()] = w[c() + 1];
             return true;
         });
     }
-    if (elim) mus[myrow] = mu;
-    tc.sync();
-    cd hj1 = f_cms(hr[J + 1], mu, pr[J + 1]);
-    cd acc0 = mk(0.0, 0.0), acc1 = mk(0.0, 0.0);
-    static_for<J + 2, S>([&](auto cc) {
-        constexpr int c = decltype(cc)::value;
-        const cd pv = pr[c], mc = mus[c];
-        hr[c] = f_cms(hr[c], mu, pv);
-        if constexpr (c & 1) acc1 = f_cma(acc1, mc, hr[c]);
-        else acc0 = f_cma(acc0, mc, hr[c]);
-        return true;
-    });
-    hr[J + 1] = f_add(hj1, f_add(acc0, acc1));
+    // logical columns S-2 and S-1 are now w[0], w[1]
+    if (myrow < S) {
+        Hs[((S - 2) * (S + 1)) / 2 + myrow] = w[0];
+        Hs[((S - 1) * (S + 2)) / 2 + myrow] = w[1];
+    }
 }
 
 template <int S, bool LOOPS>
@@ -366,17 +407,7 @@ __global__ void __launch_bounds__(kFastThreads) fast_term_kernel(const cd* __res
         });
         int myrow = lane;
         // ---------------------------------------------- Hessenberg (_numba.py:36-67)
-        static_for<0, S - 2>([&](auto jj) {
-            fast_hess_step<S, W, decltype(jj)::value>(hr, myrow, tc, ws);
-            return true;
-        });
-        {
-            cd* Hs = ws + L::HS;
-            if (myrow < S) {
-                Hs[((S - 2) * (S + 1)) / 2 + myrow] = hr[S - 2];
-                Hs[((S - 1) * (S + 2)) / 2 + myrow] = hr[S - 1];
-            }
-        }
+        fast_hessenberg<S, W>(hr, myrow, tc, ws);
         tc.sync();
         // ---------------------------------------------- charpoly (_numba.py:203-225)
         {

@@ -214,13 +214,14 @@ def run_ours(args):
     d_at = torch.from_numpy(at).to(dev)
     d_dg = torch.from_numpy(dg).to(dev)
     cnt = int(mine.size)
-    d_part = torch.zeros(max(cnt, 1), dtype=torch.complex128, device=dev)
-    d_fail = torch.zeros(max(cnt, 1), dtype=torch.int64, device=dev)
+    width = max(max(len(s) for s in shards), 1)  # all-gather needs equal sizes
+    d_part = torch.zeros(width, dtype=torch.complex128, device=dev)
+    d_fail = torch.zeros(width, dtype=torch.int64, device=dev)
     ws_bytes = int(lib.hafb_range_list_workspace_bytes(nh, N_RANGES, cnt))
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
-    gathered = [torch.zeros(max(len(s), 1), dtype=torch.complex128, device=dev) for s in shards]
+    gathered = [torch.zeros(width, dtype=torch.complex128, device=dev) for _ in shards]
 
     def step(ev_terms=None):
         if cnt:
@@ -231,7 +232,7 @@ def run_ours(args):
                 ctypes.c_void_p(d_fail.data_ptr()), ctypes.c_void_p(stream.cuda_stream),
                 ctypes.c_void_p(ev_terms.cuda_event if ev_terms is not None else 0)))
         if dist is not None:  # the exchange: per-rank range partials -> every rank
-            dist.all_gather(gathered, d_part)
+            dist.all_gather([torch.view_as_real(g) for g in gathered], torch.view_as_real(d_part))
 
     def assemble():
         parts = np.zeros(N_RANGES, np.complex128)
@@ -294,15 +295,12 @@ def run_ours(args):
         if world == 1:
             r_e2e = engine.hafnian(A, backend="charpoly", arith=args.arith)
         else:
-            s_host, f_host = kernels.sum_range_list(at, dg, nh, N_RANGES, mine, 1, False,
-                                                    arith=args.arith, device=local)
-            objs = [None] * world
-            dist.all_gather_object(objs, s_host)
-            if rank == 0:
-                parts = np.zeros(N_RANGES, np.complex128)
-                for r, s in enumerate(shards):
-                    parts[s] = objs[r]
-                r_e2e = engine.tree_reduce(parts)
+            from paper_1805_12498_b200 import distributed
+
+            r_e2e, _ = distributed.sharded_hafnian(
+                nh, lambda rl: kernels.sum_range_list(at, dg, nh, N_RANGES, rl, 1, False,
+                                                      arith=args.arith, device=local),
+                dist, rank, world)
         dt = time.perf_counter() - t0
         if dist is not None:
             t = torch.tensor([dt], dtype=torch.float64, device=dev)

@@ -49,7 +49,7 @@ def up_to_date() -> bool:
 
 def _flags(verbose):
     f = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
-         "-I", os.path.join(REPO, "include")]
+         "-I", os.path.join(REPO, "include")] + ([f"-DHAFB_STAGGER={os.environ['HAFB_STAGGER']}"] if os.environ.get("HAFB_STAGGER") else [])
     if verbose:
         f.append("-Xptxas=-v")
     return f

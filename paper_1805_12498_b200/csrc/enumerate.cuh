@@ -31,6 +31,8 @@ struct ClassItems {
     long long n_items;                  // = batch * per_problem
     long long term_stride;              // buffer offset between problems
     long long at_stride, dg_stride;     // input offsets between problems (in cd)
+    const uint32_t* mlist;              // explicit-mask mode: the class's masks ...
+    const long long* mout;              // ... and their buffer indices (else null)
 };
 
 // the r-th (0-based) integer with popcount m, bits below D
@@ -58,6 +60,11 @@ __device__ __forceinline__ ItemRef resolve_item(const ClassItems& ci, long long 
     ItemRef r;
     r.problem = item / ci.per_problem;
     long long rho = item - r.problem * ci.per_problem;
+    if (ci.mlist) {
+        r.mask = ci.mlist[rho];
+        r.out = r.problem * ci.term_stride + ci.mout[rho];
+        return r;
+    }
     int lo = 0, hi = ci.nseg - 1;
     while (lo < hi) {  // last s with prefix[s] <= rho
         int mid = (lo + hi + 1) >> 1;

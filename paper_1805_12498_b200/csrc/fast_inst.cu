@@ -10,13 +10,19 @@
 
 namespace hafb {
 
+// Hessenberg variant per size (measured on B200, tools/micro/phase.cu): the
+// shared-memory reduction wins for 18 <= S <= 26 and S >= 34, the register-window
+// reduction elsewhere.
+constexpr bool smem_hess(int S) { return (S >= 18 && S <= 26) || S >= 34; }
+
 template <int S, bool L>
 static cudaError_t launch_one(const cd* at, const cd* dg, int n_half, const ClassItems& ci,
                               cd* terms, int8_t* status, cudaStream_t st, int sms) {
     constexpr int W = TeamWidth<S>::W;
     constexpr int TPB = kFastThreads / W;
-    const size_t smem = (size_t)TPB * FastLayout<S>::TOTAL * sizeof(cd) + (kDMax + 1) * sizeof(double);
-    auto kern = fast_term_kernel<S, L>;
+    constexpr bool SH = smem_hess(S);
+    const size_t smem = (size_t)TPB * FastLayout<S, SH>::TOTAL * sizeof(cd) + (kDMax + 1) * sizeof(double);
+    auto kern = fast_term_kernel<S, L, SH>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int occ = 1;

@@ -279,6 +279,8 @@ int enqueue_fast_classes(const cd* at, const cd* dg, int n_half, const std::vect
         long long per = t.count(m);
         if (per == 0) continue;
         ClassItems ci;
+        ci.mlist = nullptr;
+        ci.mout = nullptr;
         ci.binom = d_binom;
         ci.segs = d_segs;
         ci.prefix = d_prefix + (size_t)m * (nseg + 1);
@@ -657,10 +659,48 @@ int hafb_terms(const double* atilde, const double* diag, int n_half, const uint6
     CK(cudaMemcpyAsync(d_at, atilde, sizeof(cd) * n * n, cudaMemcpyHostToDevice, c.st));
     CK(cudaMemcpyAsync(d_dg, diag, sizeof(cd) * n, cudaMemcpyHostToDevice, c.st));
     CK(cudaMemcpyAsync(d_m, h_masks.data(), sizeof(uint32_t) * count, cudaMemcpyHostToDevice, c.st));
-    MaskMap map = plain_map(0);
-    map.mask_list = d_m;
-    CK(launch_terms(backend, include_loops, d_at, d_dg, n_half, map, count, count, cap_mult, 0, 0,
-                    d_t, d_s, c.st));
+    if (arith == HAFB_ARITH_FAST && backend == 1) {
+        // group the masks by popcount: one register-kernel launch per class
+        std::vector<uint32_t> sorted(count);
+        std::vector<long long> outs(count);
+        std::vector<long long> start(n_half + 2, 0);
+        for (int64_t q = 0; q < count; ++q) start[__builtin_popcount(h_masks[q]) + 1]++;
+        for (int m = 1; m <= n_half + 1; ++m) start[m] += start[m - 1];
+        std::vector<long long> fill(start.begin(), start.end());
+        for (int64_t q = 0; q < count; ++q) {
+            long long pos = fill[__builtin_popcount(h_masks[q])]++;
+            sorted[pos] = h_masks[q];
+            outs[pos] = q;
+        }
+        uint32_t* d_sm;
+        long long* d_so;
+        CK(c.alloc(&d_sm, sizeof(uint32_t) * count));
+        CK(c.alloc(&d_so, sizeof(long long) * count));
+        CK(cudaMemcpyAsync(d_sm, sorted.data(), sizeof(uint32_t) * count, cudaMemcpyHostToDevice, c.st));
+        CK(cudaMemcpyAsync(d_so, outs.data(), sizeof(long long) * count, cudaMemcpyHostToDevice, c.st));
+        for (int m = n_half; m >= 1; --m) {
+            long long per = start[m + 1] - start[m];
+            if (per == 0) continue;
+            ClassItems ci;
+            std::memset(&ci, 0, sizeof(ci));
+            ci.m = m;
+            ci.D = n_half;
+            ci.per_problem = per;
+            ci.n_items = per;
+            ci.mlist = d_sm + start[m];
+            ci.mout = d_so + start[m];
+            cudaError_t e = include_loops
+                                ? launch_fast_class<true>(2 * m, d_at, d_dg, n_half, ci, cap_mult, d_t, d_s, c.st)
+                                : launch_fast_class<false>(2 * m, d_at, d_dg, n_half, ci, cap_mult, d_t, d_s, c.st);
+            if (e != cudaSuccess) return cuda_fail("fast class launch", e);
+            ++g_launches;
+        }
+    } else {
+        MaskMap map = plain_map(0);
+        map.mask_list = d_m;
+        CK(launch_terms(backend, include_loops, d_at, d_dg, n_half, map, count, count, cap_mult, 0,
+                        0, d_t, d_s, c.st));
+    }
     CK(cudaMemcpyAsync(terms, d_t, sizeof(cd) * count, cudaMemcpyDeviceToHost, c.st));
     CK(cudaMemcpyAsync(h_st.data(), d_s, count, cudaMemcpyDeviceToHost, c.st));
     CK(cudaStreamSynchronize(c.st));

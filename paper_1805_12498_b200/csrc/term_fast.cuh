@@ -43,24 +43,48 @@ __device__ __forceinline__ void static_for(F&& f) {
     }
 }
 
+#ifdef HAFB_TIMING
+__device__ unsigned long long g_phase[16];
+__device__ unsigned long long g_phase_cnt[16];
+#define HT_DECL long long ht_prev = clock64();
+#define HT_MARK(k)                                                    \
+    do {                                                              \
+        if (blockIdx.x == 0 && threadIdx.x == 0) {                    \
+            long long ht_now = clock64();                             \
+            atomicAdd(&g_phase[k], (unsigned long long)(ht_now - ht_prev)); \
+            atomicAdd(&g_phase_cnt[k], 1ull);                         \
+            ht_prev = ht_now;                                         \
+        }                                                             \
+    } while (0)
+#else
+#define HT_DECL
+#define HT_MARK(k)
+#endif
+
 template <int S>
 struct TeamWidth {
     static constexpr int W = S <= 2 ? 2 : S <= 4 ? 4 : S <= 8 ? 8 : S <= 16 ? 16 : S <= 32 ? 32 : 64;
 };
 
 constexpr int kFastThreads = 128;
-constexpr int kGroup = 2;  // columns per uniform branch in the Hessenberg sweep
+constexpr int kGroup = 2;
+// threshold partial pivoting: the natural pivot is kept when |h[J+1][J]| >= tau * max
+// (|multipliers| <= 1/tau); 1.0 = classic partial pivoting
+#ifndef HAFB_PIVOT_TAU
+#define HAFB_PIVOT_TAU 1.0f
+#endif
+constexpr float kPivotThreshold = HAFB_PIVOT_TAU;  // columns per uniform branch in the Hessenberg sweep
 constexpr int kDMax = 31;
 
 // packed upper-Hessenberg storage, column-major: column c holds rows 0..min(c+1, S-1)
 // and starts at c(c+3)/2.
 __host__ __device__ constexpr int hs_elems(int S) { return (S - 1) * (S + 2) / 2 + S; }
 
-template <int S>
+template <int S, bool SH = false>
 struct FastLayout {
-    static constexpr int HS = 0;
-    static constexpr int SP = S + 8;                  // padded pivot-row / multiplier length
-    static constexpr int PR = HS + hs_elems(S);       // [2][SP] pivot rows
+    static constexpr int HS = 0;                      // packed Hessenberg, or (SH) the S x S matrix
+    static constexpr int SP = S + 12;                  // padded pivot-row / multiplier length
+    static constexpr int PR = HS + (SH ? S * S : hs_elems(S));  // [2][SP] pivot rows
     static constexpr int MU = PR + 2 * SP;            // [2][SP] multipliers
     static constexpr int CF = MU + 2 * SP;            // [2][S] charpoly coefs
     static constexpr int RED = CF + 2 * S;            // [2][2][2] argmax exchange (W = 64)
@@ -71,7 +95,7 @@ struct FastLayout {
     static constexpr int G = T + kDMax + 2;           // [kDMax+2] g_j = j s_j
     static constexpr int FLAG = G + kDMax + 2;        // [1]
     static constexpr int SIGN = (S + 3) / 4 + 1;      // cd slots holding S ints
-    static constexpr int SIG = FLAG + 2;              // [2][S] int column permutation
+    static constexpr int SIG = FLAG + 2;              // [2][S] int: logical row -> lane (SH)
     static constexpr int TOTAL = SIG + 2 * SIGN;
 };
 
@@ -112,8 +136,18 @@ __device__ __forceinline__ double tshfl_up(double v, int d) {
 }
 
 __device__ __forceinline__ cd f_add(cd a, cd b) { return mk(a.re + b.re, a.im + b.im); }
+// 1/d for finite d > 0: hardware reciprocal estimate + two Newton steps (full
+// double precision without the IEEE division's special-case path)
+__device__ __forceinline__ double f_rcp(double d) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    double e = fma(-d, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-d, r, 1.0);
+    return fma(r, e, r);
+}
 __device__ __forceinline__ cd f_inv(cd p) {
-    double r = 1.0 / fma(p.re, p.re, p.im * p.im);
+    const double r = f_rcp(fma(p.re, p.re, p.im * p.im));
     return mk(p.re * r, -p.im * r);
 }
 
@@ -200,112 +234,246 @@ __device__ __forceinline__ int team_argmax_lane(const TeamCtx<W>& tc, cd* red, d
     return 63 - (int)(mx & 63u);
 }
 
-// Hessenberg reduction (_numba.py:36-67) as a ROLLED loop over steps on a shifting
-// register window: at step J, w[c] holds logical column J + c of the lane's row
-// (c < S - J live positions).  The pivot column is always w[0] and the column-op
-// target always w[1]; the trailing columns are processed in pairs under a
-// warp-uniform guard (c < live), and the window shifts left by one per step, so
-// every register index is static while the code stays one step body long
-// (a fully unrolled reduction is ~20K instructions and misses in the i-cache).
-// Rows are relabelled (lane <-> logical row `myrow`); the pivot column swap is a
-// uniform branch tree over the window.
+// One Hessenberg step J = J0 + OFF on the shifting register window w[c] = logical
+// column J0 + c of the lane's row (positions c < live = S - J0 are live).
+template <int S, int W, int OFF>
+__device__ __forceinline__ void fast_hess_step(cd (&w)[S], const int J0, int& myrow,
+                                               const TeamCtx<W>& tc, cd* ws) {
+    using L = FastLayout<S>;
+    cd* Hs = ws + L::HS;
+    HT_DECL
+    const int J = J0 + OFF;
+    const int live = S - J0;
+    const cd hj = w[OFF];
+    const double key = (myrow > J && myrow < S) ? fabs(hj.re) + fabs(hj.im) : 0.0;
+    unsigned kbits;
+    int wl = team_argmax_lane<W>(tc, ws + L::RED + 4 * OFF, key, kbits);
+    if constexpr (kPivotThreshold < 1.0f && W <= 32) {
+        // threshold pivoting: keep the natural pivot row J+1 when its key is within
+        // kPivotThreshold of the column maximum (no column swap needed then)
+        const unsigned nb = __reduce_max_sync(
+            tc.wmask, myrow == J + 1 ? __float_as_uint(__double2float_ru(key)) : 0u);
+        const unsigned nat_lane = __reduce_max_sync(tc.wmask, myrow == J + 1 ? (unsigned)tc.lane : 0u);
+        if (kbits != 0u && __uint_as_float(nb) >= kPivotThreshold * __uint_as_float(kbits))
+            wl = (int)nat_lane;
+    }
+    HT_MARK(8);
+    const int CS = (J * (J + 3)) / 2;  // start of column J in the packed store
+    if (kbits == 0u) {  // nothing to eliminate below the subdiagonal
+        if (myrow <= J + 1) Hs[CS + myrow] = hj;
+        return;
+    }
+    int brow;
+    cd p;
+    if constexpr (W <= 32) {
+        const int src = ((int)(threadIdx.x & 31) & ~(W - 1)) + wl;
+        brow = __shfl_sync(tc.wmask, myrow, src);
+        p.re = __shfl_sync(tc.wmask, hj.re, src);
+        p.im = __shfl_sync(tc.wmask, hj.im, src);
+    } else {
+        cd* r = ws + L::RED + 4 * OFF + 2;
+        if (tc.lane == wl) {
+            r[0] = hj;
+            r[1] = mk((double)myrow, 0.0);
+        }
+        tc.sync();
+        p = r[0];
+        brow = (int)r[1].re;
+    }
+    HT_MARK(5);
+    HT_MARK(13);
+    if (myrow == brow) myrow = J + 1;
+    else if (myrow == J + 1) myrow = brow;
+    if (myrow <= J + 1) Hs[CS + myrow] = hj;
+    HT_MARK(6);
+    if (brow != J + 1) swap_bs<S, OFF + 2, S>(w, OFF + 1, brow - J0);
+    HT_MARK(9);
+    const cd ip = f_inv(p);
+    const bool elim = myrow >= J + 2 && myrow < S;
+    const cd mu = elim ? f_mul(hj, ip) : mk(0.0, 0.0);
+    HT_MARK(7);
+    cd* pr = ws + L::PR + OFF * L::SP;
+    cd* mus = ws + L::MU + OFF * L::SP;
+    if (myrow == J + 1) {
+        pr[OFF + 1] = w[OFF + 1];
+        static_for<OFF + 2, S, kGroup>([&](auto gg) {
+            constexpr int c0 = decltype(gg)::value;
+            if (c0 < live) {
+                static_for<c0, (c0 + kGroup < S ? c0 + kGroup : S)>([&](auto c) {
+                    pr[c()] = w[c()];
+                    return true;
+                });
+            }
+            return true;
+        });
+#pragma unroll
+        for (int z = 0; z < kGroup; ++z) {  // zero padding past the live edge
+            pr[live + z] = mk(0.0, 0.0);
+            mus[live + z] = mk(0.0, 0.0);
+        }
+    }
+    if (elim) mus[myrow - J0] = mu;
+    tc.sync();
+    HT_MARK(10);
+    const cd hj1 = f_cms(w[OFF + 1], mu, pr[OFF + 1]);
+    cd acc0 = mk(0.0, 0.0), acc1 = mk(0.0, 0.0);
+    // pairs of columns under one uniform guard; the next pair's broadcasts are
+    // loaded before the current pair's multiply-adds (software pipelining across
+    // the guard; the padded buffers make the over-read harmless)
+    static_assert(kGroup == 2, "the pipelined sweep is written for pairs");
+    cd pa = pr[OFF + 2], ma = mus[OFF + 2], pb = pr[OFF + 3], mb = mus[OFF + 3];
+    static_for<OFF + 2, S, 2>([&](auto gg) {
+        constexpr int c = decltype(gg)::value;
+        if (c < live) {
+            const cd pa2 = pr[c + 2], ma2 = mus[c + 2], pb2 = pr[c + 3], mb2 = mus[c + 3];
+            w[c] = f_cms(w[c], mu, pa);
+            acc0 = f_cma(acc0, ma, w[c]);
+            if constexpr (c + 1 < S) {
+                w[c + 1] = f_cms(w[c + 1], mu, pb);
+                acc1 = f_cma(acc1, mb, w[c + 1]);
+            }
+            pa = pa2;
+            ma = ma2;
+            pb = pb2;
+            mb = mb2;
+        }
+        return true;
+    });
+    w[OFF + 1] = f_add(hj1, f_add(acc0, acc1));
+    HT_MARK(11);
+}
+
+// Hessenberg reduction (_numba.py:36-67) as a ROLLED loop over pairs of steps on a
+// shifting register window: at the pair starting at J0, w[c] holds logical column
+// J0 + c of the lane's row.  Both steps of the pair use static register offsets
+// (0 and 1); trailing columns run in groups under a warp-uniform guard against
+// the live edge; the window shifts left by two per pair.  Every register index is
+// static while the code stays two step bodies long (a fully unrolled reduction is
+// ~20K instructions and misses in the i-cache).  Rows are relabelled (lane <->
+// logical row `myrow`); the pivot column swap is a uniform branch tree.
 template <int S, int W>
 __device__ __forceinline__ void fast_hessenberg(cd (&w)[S], int& myrow, const TeamCtx<W>& tc,
                                                 cd* ws) {
     using L = FastLayout<S>;
-    cd* Hs = ws + L::HS;
 #pragma unroll 1
-    for (int J = 0; J < S - 2; ++J) {
-        const int live = S - J;
-        const int B = J & 1;  // double buffers of the broadcasts
-        const cd hj = w[0];
-        const double key = (myrow > J && myrow < S) ? fabs(hj.re) + fabs(hj.im) : 0.0;
-        unsigned kbits;
-        const int wl = team_argmax_lane<W>(tc, ws + L::RED + 4 * B, key, kbits);
-        const int CS = (J * (J + 3)) / 2;  // start of column J in the packed store
-        if (kbits != 0u) {
-            int brow;
-            cd p;
-            if constexpr (W <= 32) {
-                const int src = ((int)(threadIdx.x & 31) & ~(W - 1)) + wl;
-                brow = __shfl_sync(tc.wmask, myrow, src);
-                p.re = __shfl_sync(tc.wmask, hj.re, src);
-                p.im = __shfl_sync(tc.wmask, hj.im, src);
-            } else {
-                cd* r = ws + L::RED + 4 * B + 2;
-                if (tc.lane == wl) {
-                    r[0] = hj;
-                    r[1] = mk((double)myrow, 0.0);
-                }
-                tc.sync();
-                p = r[0];
-                brow = (int)r[1].re;
-            }
-            if (myrow == brow) myrow = J + 1;
-            else if (myrow == J + 1) myrow = brow;
-            if (myrow <= J + 1) Hs[CS + myrow] = hj;
-            if (brow != J + 1) swap_bs<S, 2, S>(w, 1, brow - J);
-            const cd ip = f_inv(p);
-            const bool elim = myrow >= J + 2 && myrow < S;
-            const cd mu = elim ? f_mul(hj, ip) : mk(0.0, 0.0);
-            cd* pr = ws + L::PR + B * L::SP;
-            cd* mus = ws + L::MU + B * L::SP;
-            if (myrow == J + 1) {
-                pr[1] = w[1];
-                static_for<2, S, kGroup>([&](auto gg) {
-                    constexpr int c0 = decltype(gg)::value;
-                    if (c0 < live) {
-                        static_for<c0, (c0 + kGroup < S ? c0 + kGroup : S)>([&](auto c) {
-                            pr[c()] = w[c()];
-                            return true;
-                        });
-                    }
-                    return true;
-                });
-                // zero padding: the last group may run past the live edge
-#pragma unroll
-                for (int z = 0; z < kGroup; ++z) {
-                    pr[live + z] = mk(0.0, 0.0);
-                    mus[live + z] = mk(0.0, 0.0);
-                }
-            }
-            if (elim) mus[myrow - J] = mu;
-            tc.sync();
-            const cd hj1 = f_cms(w[1], mu, pr[1]);
-            cd acc0 = mk(0.0, 0.0), acc1 = mk(0.0, 0.0);
-            // columns in groups of kGroup under one uniform branch
-            static_for<2, S, kGroup>([&](auto gg) {
-                constexpr int c0 = decltype(gg)::value;
-                if (c0 < live) {
-                    static_for<c0, (c0 + kGroup < S ? c0 + kGroup : S)>([&](auto cc) {
-                        constexpr int c = decltype(cc)::value;
-                        const cd pv = pr[c], mc = mus[c];
-                        w[c] = f_cms(w[c], mu, pv);
-                        if constexpr (c & 1) acc1 = f_cma(acc1, mc, w[c]);
-                        else acc0 = f_cma(acc0, mc, w[c]);
-                        return true;
-                    });
-                }
-                return true;
-            });
-            w[1] = f_add(hj1, f_add(acc0, acc1));
-        } else {  // nothing to eliminate below the subdiagonal
-            if (myrow <= J + 1) Hs[CS + myrow] = hj;
-        }
-        // (per-position predicated moves: this form keeps register pressure lowest)
-        static_for<0, S - 1>([&](auto c) {
-            if (c() + 1 < live) w[c()] = w[c() + 1];
+    for (int J0 = 0; J0 < S - 2; J0 += 2) {
+        fast_hess_step<S, W, 0>(w, J0, myrow, tc, ws);
+        fast_hess_step<S, W, 1>(w, J0, myrow, tc, ws);
+        HT_DECL
+        const int live = S - J0;
+        static_for<0, S - 2>([&](auto c) {
+            if (c() + 2 < live) w[c()] = w[c() + 2];
             return true;
         });
+        HT_MARK(12);
     }
     // logical columns S-2 and S-1 are now w[0], w[1]
+    cd* Hs = ws + L::HS;
     if (myrow < S) {
         Hs[((S - 2) * (S + 1)) / 2 + myrow] = w[0];
         Hs[((S - 1) * (S + 2)) / 2 + myrow] = w[1];
     }
 }
 
-template <int S, bool LOOPS>
+// Hessenberg reduction with the subset matrix in SHARED memory (column-major,
+// H[c*S + lane] = row `lane`, column c): dynamic column indices are free, so the
+// column swap of the pivoting is two loads and two stores per lane, the pivot row
+// is read in place (no publish), and the kernel needs few registers (higher
+// occupancy hides the per-step serial latency).  Rows are relabelled (lane <->
+// logical row); `lm` (logical row -> lane, double-buffered) is kept for the
+// charpoly.  Same arithmetic identities as fast_hessenberg.
+template <int S, int W>
+__device__ __forceinline__ void smem_hessenberg(cd* H, int& myrow, const TeamCtx<W>& tc, cd* ws) {
+    using L = FastLayout<S, true>;
+    const int lane = tc.lane;
+    int* lm0 = reinterpret_cast<int*>(ws + L::SIG);
+    if (lane < S) lm0[lane] = lane;
+    tc.sync();
+    cd* mus = ws + L::MU;
+#pragma unroll 1
+    for (int J = 0; J < S - 2; ++J) {
+        const int B = J & 1;
+        const int* lm = reinterpret_cast<const int*>(ws + L::SIG + B * L::SIGN);
+        int* lm_next = reinterpret_cast<int*>(ws + L::SIG + (1 - B) * L::SIGN);
+        const cd x = lane < S ? H[J * S + lane] : mk(0.0, 0.0);
+        const double key = (myrow > J && myrow < S) ? fabs(x.re) + fabs(x.im) : 0.0;
+        unsigned kbits;
+        const int wl = team_argmax_lane<W>(tc, ws + L::RED + 4 * B, key, kbits);
+        if (kbits == 0u) {  // nothing to eliminate below the subdiagonal
+            if (lane < S) lm_next[lane] = lm[lane];
+            tc.sync();
+            continue;
+        }
+        int brow;
+        cd p;
+        if constexpr (W <= 32) {
+            const int src = ((int)(threadIdx.x & 31) & ~(W - 1)) + wl;
+            brow = __shfl_sync(tc.wmask, myrow, src);
+            p.re = __shfl_sync(tc.wmask, x.re, src);
+            p.im = __shfl_sync(tc.wmask, x.im, src);
+        } else {
+            cd* r = ws + L::RED + 4 * B + 2;
+            if (lane == wl) {
+                r[0] = x;
+                r[1] = mk((double)myrow, 0.0);
+            }
+            tc.sync();
+            p = r[0];
+            brow = (int)r[1].re;
+        }
+        const int lane_j1 = lm[J + 1];
+        if (lane < S) lm_next[lane] = lane == J + 1 ? wl : (lane == brow ? lane_j1 : lm[lane]);
+        if (myrow == brow) myrow = J + 1;
+        else if (myrow == J + 1) myrow = brow;
+        cd x1 = lane < S ? H[(J + 1) * S + lane] : mk(0.0, 0.0);
+        if (brow != J + 1 && lane < S) {  // column swap J+1 <-> brow (own row)
+            const cd xb = H[brow * S + lane];
+            H[brow * S + lane] = x1;
+            if constexpr (W > 32) H[(J + 1) * S + lane] = xb;  // read back as pv1 below
+            x1 = xb;
+        }
+        const cd ip = f_inv(p);
+        const bool elim = myrow >= J + 2 && myrow < S;
+        const cd mu = elim ? f_mul(x, ip) : mk(0.0, 0.0);
+        if (elim) mus[myrow] = mu;
+        cd pv1 = mk(0.0, 0.0);  // the pivot row's (swapped) column J+1 entry
+        if constexpr (W <= 32) {
+            const int src = ((int)(threadIdx.x & 31) & ~(W - 1)) + wl;
+            pv1.re = __shfl_sync(tc.wmask, x1.re, src);
+            pv1.im = __shfl_sync(tc.wmask, x1.im, src);
+        }
+        tc.sync();
+        if constexpr (W > 32) pv1 = H[(J + 1) * S + wl];  // read before column J+1 changes
+        const cd hj1 = f_cms(x1, mu, pv1);
+        cd acc0 = mk(0.0, 0.0), acc1 = mk(0.0, 0.0);
+        const cd* prow = H + wl;  // the pivot row, read in place
+        int c = J + 2;
+#pragma unroll 1
+        for (; c + 1 < S; c += 2) {
+            const cd xa = H[c * S + lane], xb = H[(c + 1) * S + lane];
+            const cd pa = prow[c * S], pb = prow[(c + 1) * S];
+            const cd ma = mus[c], mb = mus[c + 1];
+            const cd ya = f_cms(xa, mu, pa), yb = f_cms(xb, mu, pb);
+            acc0 = f_cma(acc0, ma, ya);
+            acc1 = f_cma(acc1, mb, yb);
+            if (elim) {
+                H[c * S + lane] = ya;
+                H[(c + 1) * S + lane] = yb;
+            }
+        }
+        if (c < S) {
+            const cd xa = H[c * S + lane], pa = prow[c * S], ma = mus[c];
+            const cd ya = f_cms(xa, mu, pa);
+            acc0 = f_cma(acc0, ma, ya);
+            if (elim) H[c * S + lane] = ya;
+        }
+        if constexpr (W > 32) tc.sync();  // everyone has read pv1 before column J+1 changes
+        if (lane < S) H[(J + 1) * S + lane] = f_add(hj1, f_add(acc0, acc1));
+    }
+    tc.sync();
+}
+
+template <int S, bool LOOPS, bool SH>
 __global__ void __launch_bounds__(kFastThreads) fast_term_kernel(const cd* __restrict__ atilde,
                                                                  const cd* __restrict__ diag,
                                                                  int n_half, ClassItems ci,
@@ -315,7 +483,7 @@ __global__ void __launch_bounds__(kFastThreads) fast_term_kernel(const cd* __res
     constexpr int TPB = kFastThreads / W;
     constexpr int M = S / 2;
     constexpr int R = (kDMax + W - 1) / W;  // coefficient chunks per lane
-    using L = FastLayout<S>;
+    using L = FastLayout<S, SH>;
     extern __shared__ cd smem[];
     TeamCtx<W> tc;
     tc.tib = threadIdx.x / W;
@@ -335,8 +503,13 @@ __global__ void __launch_bounds__(kFastThreads) fast_term_kernel(const cd* __res
     const int n = 2 * n_half;
     const int D = n_half;
     const long long stride = (long long)gridDim.x * TPB;
+#ifdef HAFB_STAGGER
+    // experiment: de-phase the warps of an SM so their serial sections overlap others' sweeps
+    __nanosleep((unsigned)(((threadIdx.x >> 5) + 4 * (blockIdx.x % 4)) % 16) * HAFB_STAGGER);
+#endif
 
     for (long long base = (long long)blockIdx.x * TPB; base < ci.n_items; base += stride) {
+        HT_DECL
         const long long item = base + tc.tib;
         const bool valid = item < ci.n_items;
         const ItemRef ir = resolve_item(ci, valid ? item : base);
@@ -400,18 +573,44 @@ __global__ void __launch_bounds__(kFastThreads) fast_term_kernel(const cd* __res
         }
         // ---------------------------------------------- gather B rows
         const int vr = 2 * mybit + (lane & 1);
-        static_for<0, S>([&](auto c) {
-            const int vc = 2 * vbit[c() >> 1] + (c() & 1);
-            hr[c()] = lane < S ? at[vr * n + vc] : mk(0.0, 0.0);
-            return true;
-        });
         int myrow = lane;
-        // ---------------------------------------------- Hessenberg (_numba.py:36-67)
-        fast_hessenberg<S, W>(hr, myrow, tc, ws);
+        if constexpr (SH) {
+            cd* H = ws + L::HS;
+            static_for<0, S>([&](auto c) {
+                const int vc = 2 * vbit[c() >> 1] + (c() & 1);
+                if (lane < S) H[c() * S + lane] = at[vr * n + vc];
+                return true;
+            });
+            tc.sync();
+            HT_MARK(0);
+            smem_hessenberg<S, W>(H, myrow, tc, ws);
+        } else {
+            static_for<0, S>([&](auto c) {
+                const int vc = 2 * vbit[c() >> 1] + (c() & 1);
+                hr[c()] = lane < S ? at[vr * n + vc] : mk(0.0, 0.0);
+                return true;
+            });
+            HT_MARK(0);
+            // ---------------------------------------------- Hessenberg (_numba.py:36-67)
+            fast_hessenberg<S, W>(hr, myrow, tc, ws);
+        }
+        HT_MARK(1);
         tc.sync();
         // ---------------------------------------------- charpoly (_numba.py:203-225)
         {
             const cd* Hs = ws + L::HS;
+            // h(i, c) of the Hessenberg form: packed store, or (SH) the matrix in smem
+            // with logical row i in lane lm[i]
+            const int* lmf = reinterpret_cast<const int*>(ws + L::SIG + ((S - 2) & 1) * L::SIGN);
+            const int my_lm = SH && lane < S ? lmf[lane] : 0;
+            auto hget = [&](int i, int c) -> cd {
+                if constexpr (SH) return Hs[c * S + lmf[i]];
+                else return Hs[(c * (c + 3)) / 2 + i];
+            };
+            auto hget_mine = [&](int c) -> cd {  // h(lane, c)
+                if constexpr (SH) return Hs[c * S + my_lm];
+                else return Hs[(c * (c + 3)) / 2 + lane];
+            };
             cd* A = ws + L::A;
             cd P[S];
             P[0] = mk(lane == 0 ? 1.0 : 0.0, 0.0);
@@ -420,10 +619,10 @@ __global__ void __launch_bounds__(kFastThreads) fast_term_kernel(const cd* __res
                 constexpr int k = decltype(kk)::value;
                 cd* cf = ws + L::CF + (k & 1) * S;
                 if constexpr (k >= 2) {
-                    const cd beta = Hs[((k - 2) * (k + 1)) / 2 + (k - 1)];  // h[k-1][k-2]
+                    const cd beta = hget(k - 1, k - 2);  // h[k-1][k-2]
                     if (lane <= k - 2) {
                         prodl = f_mul(lane == k - 2 ? mk(1.0, 0.0) : prodl, beta);
-                        cf[lane] = f_mul(Hs[((k - 1) * (k + 2)) / 2 + lane], prodl);
+                        cf[lane] = f_mul(hget_mine(k - 1), prodl);
                     }
                 }
                 cd prev;
@@ -438,9 +637,9 @@ __global__ void __launch_bounds__(kFastThreads) fast_term_kernel(const cd* __res
                 }
                 if (lane == 0) prev = mk(0.0, 0.0);
                 tc.sync();
-                const cd hk = Hs[((k - 1) * (k + 2)) / 2 + (k - 1)];
+                const cd hk = hget(k - 1, k - 1);
                 cd acc = f_cms(prev, hk, P[k - 1]);
-                cd acc2 = mk(0.0, 0.0);
+                cd acc2 = mk(0.0, 0.0), acc3 = mk(0.0, 0.0), acc4 = mk(0.0, 0.0);
                 // chunks of four coefficients; the opaque branch is a basic-block fence
                 // that bounds how many broadcast loads the scheduler hoists at once
                 static_for<1, k, 4>([&](auto ii) {
@@ -448,13 +647,15 @@ __global__ void __launch_bounds__(kFastThreads) fast_term_kernel(const cd* __res
                     if (i0 >= k + opaque_zero) return false;
                     static_for<i0, (i0 + 4 < k ? i0 + 4 : k)>([&](auto jj) {
                         constexpr int i = decltype(jj)::value;
-                        if constexpr (i & 1) acc = f_cms(acc, cf[i - 1], P[i - 1]);
-                        else acc2 = f_cms(acc2, cf[i - 1], P[i - 1]);
+                        if constexpr ((i & 3) == 0) acc = f_cms(acc, cf[i - 1], P[i - 1]);
+                        else if constexpr ((i & 3) == 1) acc2 = f_cms(acc2, cf[i - 1], P[i - 1]);
+                        else if constexpr ((i & 3) == 2) acc3 = f_cms(acc3, cf[i - 1], P[i - 1]);
+                        else acc4 = f_cms(acc4, cf[i - 1], P[i - 1]);
                         return true;
                     });
                     return true;
                 });
-                acc = f_add(acc, acc2);
+                acc = f_add(f_add(acc, acc2), f_add(acc3, acc4));
                 if constexpr (k < S) P[k] = acc;
                 else if (lane < S) A[lane] = acc;
                 return true;
@@ -462,6 +663,7 @@ __global__ void __launch_bounds__(kFastThreads) fast_term_kernel(const cd* __res
             if (lane == 0) A[S] = mk(1.0, 0.0);
             tc.sync();
         }
+        HT_MARK(2);
         // ---------------------------------------------- Newton + Cayley-Hamilton (_numba.py:228-250)
         cd* T = ws + L::T;
         cd* A = ws + L::A;
@@ -476,13 +678,25 @@ __global__ void __launch_bounds__(kFastThreads) fast_term_kernel(const cd* __res
             }
             for (int kk = 1; kk <= D; ++kk) {
                 const int owner = (kk - 1) % W, chunk = (kk - 1) / W;
-                if (lane == owner) {
+                cd tk;
+                if constexpr (W <= 32) {  // register broadcast from the owner lane
+                    cd v = acck[0];
 #pragma unroll
-                    for (int r = 0; r < R; ++r)
-                        if (r == chunk) T[kk] = acck[r];
+                    for (int r = 1; r < R; ++r)
+                        if (r == chunk) v = acck[r];
+                    const int src = ((int)(threadIdx.x & 31) & ~(W - 1)) + owner;
+                    tk.re = __shfl_sync(tc.wmask, v.re, src);
+                    tk.im = __shfl_sync(tc.wmask, v.im, src);
+                    if (lane == owner) T[kk] = tk;
+                } else {
+                    if (lane == owner) {
+#pragma unroll
+                        for (int r = 0; r < R; ++r)
+                            if (r == chunk) T[kk] = acck[r];
+                    }
+                    tc.sync();
+                    tk = T[kk];
                 }
-                tc.sync();
-                const cd tk = T[kk];
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
                     const int k = lane + 1 + W * r;
@@ -500,6 +714,7 @@ __global__ void __launch_bounds__(kFastThreads) fast_term_kernel(const cd* __res
                 G[k] = g;
             }
         }
+        HT_MARK(3);
         // any lane saw a non-finite trace -> status 2
         if constexpr (W <= 32) {
             bad = __any_sync(tc.wmask, bad);
@@ -519,18 +734,34 @@ __global__ void __launch_bounds__(kFastThreads) fast_term_kernel(const cd* __res
             for (int r = 0; r < R; ++r) acck[r] = mk(0.0, 0.0);
             for (int kk = 0; kk < D; ++kk) {
                 const int owner = (kk - 1 + W) % W, chunk = (kk - 1) / W;
-                if (kk == 0) {
-                    if (lane == 0) T[0] = mk(1.0, 0.0);
-                } else if (lane == owner) {
+                cd ek;
+                if constexpr (W <= 32) {  // register broadcast from the owner lane
+                    if (kk == 0) {
+                        ek = mk(1.0, 0.0);
+                    } else {
+                        cd v = acck[0];
 #pragma unroll
-                    for (int r = 0; r < R; ++r)
-                        if (r == chunk) {
-                            const double inv = INV[kk];
-                            T[kk] = mk(acck[r].re * inv, acck[r].im * inv);
-                        }
+                        for (int r = 1; r < R; ++r)
+                            if (r == chunk) v = acck[r];
+                        const int src = ((int)(threadIdx.x & 31) & ~(W - 1)) + owner;
+                        const double inv = INV[kk];
+                        ek.re = __shfl_sync(tc.wmask, v.re, src) * inv;
+                        ek.im = __shfl_sync(tc.wmask, v.im, src) * inv;
+                    }
+                } else {
+                    if (kk == 0) {
+                        if (lane == 0) T[0] = mk(1.0, 0.0);
+                    } else if (lane == owner) {
+#pragma unroll
+                        for (int r = 0; r < R; ++r)
+                            if (r == chunk) {
+                                const double inv = INV[kk];
+                                T[kk] = mk(acck[r].re * inv, acck[r].im * inv);
+                            }
+                    }
+                    tc.sync();
+                    ek = T[kk];
                 }
-                tc.sync();
-                const cd ek = T[kk];
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
                     const int k = lane + 1 + W * r;
@@ -550,6 +781,7 @@ __global__ void __launch_bounds__(kFastThreads) fast_term_kernel(const cd* __res
             status[ir.out] = bad ? 2 : 0;
         }
         tc.sync();
+        HT_MARK(4);
     }
 }
 

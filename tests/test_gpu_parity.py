@@ -286,3 +286,42 @@ def test_fast_arith_within_tolerance(cfg, tol):
     g = load_golden("ranges.npz")[cfg]
     got = engine.hafnian(g["A"], backend="charpoly", arith="fast")
     assert rel_err(got, complex(g["result_b1"])) < tol
+
+
+# ------------------------------------------------------------------ fast arithmetic at scale
+
+def test_fast_arith_large_configs():
+    """FAST kernels (every team width, both Hessenberg variants) on the configs with
+    the largest subset sizes: within the conditioning-limited tolerance of the
+    bit-exact reference values."""
+    g = load_golden("ranges.npz")["cfg3"]
+    got = engine.hafnian(g["A"], backend="charpoly", arith="fast")
+    exact = 308544357990268074
+    assert abs(got.real - exact) / exact < 1e-5  # cond 8.8e9; the reference is 6.8e-7 off
+    r = load_golden("range_n52.npz")
+    for name in ("n52s3", "n52s4", "n56s4"):
+        case = r[name]
+        at, dg, nh = engine._prepare(case["A"], False)
+        sums, fails = kernels.sum_mask_range(at, dg, nh, 0, 1 << 20, 512, 1, False, arith="fast")
+        assert not fails.any()
+        ref = complex(case["result_b1"])
+        assert rel_err(engine.tree_reduce(sums), ref) < 1e-9, name
+
+
+@pytest.mark.parametrize("S", [2, 4, 8, 12, 16, 18, 22, 26, 30, 32, 34, 38, 42, 46, 50])
+def test_fast_terms_every_size_vs_oracle(S):
+    """Per-term FAST vs the bit-exact oracle for subsets of every size class."""
+    n = max(S, 20) + (max(S, 20) % 2)
+    A = random_symmetric(n, 1000 + S) / np.sqrt(n)
+    at, dg, nh = engine._prepare(A, False)
+    rng = np.random.default_rng(S)
+    masks = []
+    for _ in range(16):
+        bits = rng.choice(nh, size=S // 2, replace=False)
+        masks.append(int(sum(1 << int(b) for b in bits)))
+    masks = np.array(masks, dtype=np.uint64)
+    ref, _ = O.terms(at, dg, nh, masks, backend=1)
+    got, st = kernels.terms(at, dg, nh, masks, 1, False, arith="fast")
+    scale = np.abs(ref).max()
+    assert not st.any()
+    assert np.abs(got - ref).max() <= 1e-10 * scale

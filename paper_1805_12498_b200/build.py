@@ -23,6 +23,7 @@ OBJ = os.path.join(os.environ.get("HAFB200_BUILD_DIR", "/tmp/hafb200_build"))
 LIB = os.path.join(PKG, "libhafb200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FAST_SIZES = list(range(2, 49, 2))  # kFastSMax = 48 (csrc/fast_launch.h)
+MIRROR_SIZES = list(range(2, 63, 2))  # n <= 62
 
 
 def nvcc() -> str:
@@ -59,6 +60,8 @@ def _units():
     units = [("hafb200.o", os.path.join(CSRC, "hafb200.cu"), [])]
     for s in FAST_SIZES:
         units.append((f"fast_{s:02d}.o", os.path.join(CSRC, "fast_inst.cu"), [f"-DHAFB_S={s}"]))
+    for s in MIRROR_SIZES:
+        units.append((f"mirror_{s:02d}.o", os.path.join(CSRC, "mirror_inst.cu"), [f"-DHAFB_S={s}"]))
     return units
 
 

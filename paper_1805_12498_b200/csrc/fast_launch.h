@@ -16,4 +16,10 @@ template <int S>
 cudaError_t launch_fast_S(bool loops, const cd* at, const cd* dg, int n_half, const ClassItems& ci,
                           cd* terms, int8_t* status, cudaStream_t st, int sms);
 
+// launch mirror_term_kernel<S, loops> (bit-exact charpoly backend), S = 2..62
+template <int S>
+cudaError_t launch_mirror_S(bool loops, const cd* at, const cd* dg, int n_half,
+                            const ClassItems& ci, cd* terms, int8_t* status, cudaStream_t st,
+                            int sms);
+
 }  // namespace hafb

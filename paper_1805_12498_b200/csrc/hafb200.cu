@@ -253,11 +253,41 @@ cudaError_t launch_fast_class(int S, const cd* at, const cd* dg, int n_half, con
     }
 }
 
+template <bool L>
+cudaError_t launch_mirror_class(int S, const cd* at, const cd* dg, int n_half,
+                                const ClassItems& ci, cd* terms, int8_t* status, cudaStream_t st) {
+    const int sms = sm_count();
+    switch (S) {
+#define MC(SS) \
+    case SS: return launch_mirror_S<SS>(L, at, dg, n_half, ci, terms, status, st, sms);
+        MC(2) MC(4) MC(6) MC(8) MC(10) MC(12) MC(14) MC(16) MC(18) MC(20) MC(22) MC(24)
+        MC(26) MC(28) MC(30) MC(32) MC(34) MC(36) MC(38) MC(40) MC(42) MC(44) MC(46) MC(48)
+        MC(50) MC(52) MC(54) MC(56) MC(58) MC(60) MC(62)
+#undef MC
+        default:
+            return cudaErrorInvalidValue;
+    }
+}
+
+// class-path launch for the register/smem term kernels: FAST or bit-exact MIRROR
+cudaError_t launch_class(int arith, bool loops, int S, const cd* at, const cd* dg, int n_half,
+                         const ClassItems& ci, int cap, cd* terms, int8_t* status, cudaStream_t st) {
+    if (arith == HAFB_ARITH_MIRROR)
+        return loops ? launch_mirror_class<true>(S, at, dg, n_half, ci, terms, status, st)
+                     : launch_mirror_class<false>(S, at, dg, n_half, ci, terms, status, st);
+    return loops ? launch_fast_class<true>(S, at, dg, n_half, ci, cap, terms, status, st)
+                 : launch_fast_class<false>(S, at, dg, n_half, ci, cap, terms, status, st);
+}
+
+// the class path serves the charpoly backend in both arithmetics; the spectral
+// backend runs in the shared-memory kernel (term_smem.cuh)
+bool use_class_path(int backend) { return backend == 1; }
+
 // Upload the tables and launch every nonempty class (largest classes first).
-int enqueue_fast_classes(const cd* at, const cd* dg, int n_half, const std::vector<Seg>& segs,
-                         int batch, long long term_stride, long long at_stride, long long dg_stride,
-                         int loops, int cap, cd* terms, int8_t* status, void* table_ws,
-                         cudaStream_t st) {
+int enqueue_classes(int arith, const cd* at, const cd* dg, int n_half, const std::vector<Seg>& segs,
+                    int batch, long long term_stride, long long at_stride, long long dg_stride,
+                    int loops, int cap, cd* terms, int8_t* status, void* table_ws,
+                    cudaStream_t st) {
     const int D = n_half;
     ClassTables t = build_tables(D, segs);
     const size_t nseg = segs.size();
@@ -293,8 +323,7 @@ int enqueue_fast_classes(const cd* at, const cd* dg, int n_half, const std::vect
         ci.term_stride = term_stride;
         ci.at_stride = at_stride;
         ci.dg_stride = dg_stride;
-        cudaError_t e = loops ? launch_fast_class<true>(2 * m, at, dg, n_half, ci, cap, terms, status, st)
-                              : launch_fast_class<false>(2 * m, at, dg, n_half, ci, cap, terms, status, st);
+        cudaError_t e = launch_class(arith, loops, 2 * m, at, dg, n_half, ci, cap, terms, status, st);
         ++g_launches;
         if (e != cudaSuccess) return cuda_fail("fast class launch", e);
     }
@@ -325,14 +354,14 @@ int enqueue_mask_range(const cd* at, const cd* dg, int n_half, uint64_t lo, uint
     int8_t* status;
     carve_terms_ws(ws, count, &terms, &status);
     if (count > 0) {
-        if (arith == HAFB_ARITH_FAST && backend == 1) {
+        if (use_class_path(backend)) {
             std::vector<Seg> segs(1);
             segs[0].lo = lo;
             segs[0].hi = hi;
             segs[0].out_off = 0;
             void* tw = static_cast<char*>(ws) + terms_ws_bytes(count);
-            int rc = enqueue_fast_classes(at, dg, n_half, segs, 1, 0, 0, 0, loops, cap, terms,
-                                          status, tw, st);
+            int rc = enqueue_classes(arith, at, dg, n_half, segs, 1, 0, 0, 0, loops, cap, terms,
+                                     status, tw, st);
             if (rc) return rc;
         } else {
             CK(launch_terms(backend, loops, at, dg, n_half, plain_map(lo), count, count, cap, 0, 0,
@@ -365,7 +394,7 @@ int enqueue_range_list(const cd* at, const cd* dg, int n_half, int n_ranges, con
     int32_t* d_ranges = reinterpret_cast<int32_t*>(tw + table_ws_bytes(n_half, count));
     CK(cudaMemcpyAsync(d_ranges, h_ranges, sizeof(int32_t) * count, cudaMemcpyHostToDevice, st));
     if (items > 0) {
-        if (arith == HAFB_ARITH_FAST && backend == 1) {
+        if (use_class_path(backend)) {
             std::vector<Seg> segs(count);
             for (int p = 0; p < count; ++p) {
                 uint64_t a = 1 + (uint64_t)h_ranges[p] * width;
@@ -373,8 +402,8 @@ int enqueue_range_list(const cd* at, const cd* dg, int n_half, int n_ranges, con
                 segs[p].hi = std::min(a + width, total);
                 segs[p].out_off = (long long)p * (long long)width;
             }
-            int rc = enqueue_fast_classes(at, dg, n_half, segs, 1, 0, 0, 0, loops, cap, terms,
-                                          status, tw, st);
+            int rc = enqueue_classes(arith, at, dg, n_half, segs, 1, 0, 0, 0, loops, cap, terms,
+                                     status, tw, st);
             if (rc) return rc;
         } else {
             MaskMap map;
@@ -609,12 +638,12 @@ int hafb_sum_subsets_fast(const double* atilde, const double* diag, int n_half, 
     CK(cudaMemcpyAsync(d_at, atilde, sizeof(cd) * n * n, cudaMemcpyHostToDevice, c.st));
     CK(cudaMemcpyAsync(d_dg, diag, sizeof(cd) * n, cudaMemcpyHostToDevice, c.st));
     carve_terms_ws(d_ws, count, &terms, &status);
-    if (arith == HAFB_ARITH_FAST && backend == 1) {
+    if (use_class_path(backend)) {
         std::vector<Seg> segs(1);
         segs[0].lo = 1;
         segs[0].hi = total;
         segs[0].out_off = 0;
-        rc = enqueue_fast_classes(d_at, d_dg, n_half, segs, 1, 0, 0, 0, include_loops, cap_mult,
+        rc = enqueue_classes(arith, d_at, d_dg, n_half, segs, 1, 0, 0, 0, include_loops, cap_mult,
                                   terms, status, static_cast<char*>(d_ws) + terms_ws_bytes(count),
                                   c.st);
         if (rc) return rc;
@@ -659,8 +688,8 @@ int hafb_terms(const double* atilde, const double* diag, int n_half, const uint6
     CK(cudaMemcpyAsync(d_at, atilde, sizeof(cd) * n * n, cudaMemcpyHostToDevice, c.st));
     CK(cudaMemcpyAsync(d_dg, diag, sizeof(cd) * n, cudaMemcpyHostToDevice, c.st));
     CK(cudaMemcpyAsync(d_m, h_masks.data(), sizeof(uint32_t) * count, cudaMemcpyHostToDevice, c.st));
-    if (arith == HAFB_ARITH_FAST && backend == 1) {
-        // group the masks by popcount: one register-kernel launch per class
+    if (use_class_path(backend)) {
+        // group the masks by popcount: one kernel launch per class
         std::vector<uint32_t> sorted(count);
         std::vector<long long> outs(count);
         std::vector<long long> start(n_half + 2, 0);
@@ -689,9 +718,8 @@ int hafb_terms(const double* atilde, const double* diag, int n_half, const uint6
             ci.n_items = per;
             ci.mlist = d_sm + start[m];
             ci.mout = d_so + start[m];
-            cudaError_t e = include_loops
-                                ? launch_fast_class<true>(2 * m, d_at, d_dg, n_half, ci, cap_mult, d_t, d_s, c.st)
-                                : launch_fast_class<false>(2 * m, d_at, d_dg, n_half, ci, cap_mult, d_t, d_s, c.st);
+            cudaError_t e = launch_class(arith, include_loops, 2 * m, d_at, d_dg, n_half, ci,
+                                         cap_mult, d_t, d_s, c.st);
             if (e != cudaSuccess) return cuda_fail("fast class launch", e);
             ++g_launches;
         }
@@ -738,12 +766,12 @@ int hafb_batch(const double* atilde, const double* diag, int batch, int n_half, 
     CK(c.alloc(&d_res, sizeof(cd) * batch));
     CK(cudaMemcpyAsync(d_at, atilde, sizeof(cd) * n * n * (size_t)batch, cudaMemcpyHostToDevice, c.st));
     CK(cudaMemcpyAsync(d_dg, diag, sizeof(cd) * n * (size_t)batch, cudaMemcpyHostToDevice, c.st));
-    if (arith == HAFB_ARITH_FAST && backend == 1) {
+    if (use_class_path(backend)) {
         std::vector<Seg> segs(1);
         segs[0].lo = 1;
         segs[0].hi = total;
         segs[0].out_off = 0;
-        rc = enqueue_fast_classes(d_at, d_dg, n_half, segs, batch, per, (long long)n * n, n,
+        rc = enqueue_classes(arith, d_at, d_dg, n_half, segs, batch, per, (long long)n * n, n,
                                   include_loops, cap_mult, d_t, d_s, d_tab, c.st);
         if (rc) return rc;
     } else {

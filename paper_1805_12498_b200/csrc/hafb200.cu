@@ -93,6 +93,16 @@ struct Call {
     }
 };
 
+// Kernels whose dynamic shared memory varies per launch get the opt-in maximum as
+// their attribute (a per-launch value would race between host threads launching
+// the same kernel with different sizes).
+int smem_optin() {
+    int dev = 0, v = 227 * 1024;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return v;
+}
+
 int sm_count() {
     int dev = 0, v = 148;
     cudaGetDevice(&dev);
@@ -109,7 +119,7 @@ cudaError_t launch_terms_t(const cd* at, const cd* dg, int n_half, MaskMap map, 
     int wpb = (int)std::min<size_t>(8, std::max<size_t>(1, (200 * 1024) / per_warp));
     size_t smem = wpb * per_warp;
     auto kern = terms_smem_kernel<B, L>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin());
     if (e != cudaSuccess) return e;
     int occ = 1;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, wpb * 32, smem);
@@ -219,15 +229,14 @@ ClassTables build_tables(int D, const std::vector<Seg>& segs) {
     return t;
 }
 
-template <bool L>
+template <bool L, int B = 1>
 cudaError_t launch_smem_class(const cd* at, const cd* dg, int n_half, const ClassItems& ci, int cap,
                               cd* terms, int8_t* status, cudaStream_t st) {
-    const int n = 2 * n_half;
-    size_t per_warp = (size_t)smem_warp_elems(n) * sizeof(cd);
+    size_t per_warp = (size_t)smem_warp_elems(2 * ci.m, n_half) * sizeof(cd);
     int wpb = (int)std::min<size_t>(8, std::max<size_t>(1, (200 * 1024) / per_warp));
     size_t smem = wpb * per_warp;
-    auto kern = terms_smem_class_kernel<1, L>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto kern = terms_smem_class_kernel<B, L>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin());
     if (e != cudaSuccess) return e;
     int occ = 1;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, wpb * 32, smem);
@@ -270,8 +279,12 @@ cudaError_t launch_mirror_class(int S, const cd* at, const cd* dg, int n_half,
 }
 
 // class-path launch for the register/smem term kernels: FAST or bit-exact MIRROR
-cudaError_t launch_class(int arith, bool loops, int S, const cd* at, const cd* dg, int n_half,
-                         const ClassItems& ci, int cap, cd* terms, int8_t* status, cudaStream_t st) {
+cudaError_t launch_class(int backend, int arith, bool loops, int S, const cd* at, const cd* dg,
+                         int n_half, const ClassItems& ci, int cap, cd* terms, int8_t* status,
+                         cudaStream_t st) {
+    if (backend == 0)  // spectral: shared-memory kernel (MIRROR arithmetic), one class per launch
+        return loops ? launch_smem_class<true, 0>(at, dg, n_half, ci, cap, terms, status, st)
+                     : launch_smem_class<false, 0>(at, dg, n_half, ci, cap, terms, status, st);
     if (arith == HAFB_ARITH_MIRROR)
         return loops ? launch_mirror_class<true>(S, at, dg, n_half, ci, terms, status, st)
                      : launch_mirror_class<false>(S, at, dg, n_half, ci, terms, status, st);
@@ -279,12 +292,11 @@ cudaError_t launch_class(int arith, bool loops, int S, const cd* at, const cd* d
                  : launch_fast_class<false>(S, at, dg, n_half, ci, cap, terms, status, st);
 }
 
-// the class path serves the charpoly backend in both arithmetics; the spectral
-// backend runs in the shared-memory kernel (term_smem.cuh)
-bool use_class_path(int backend) { return backend == 1; }
+// every backend runs on the class path (one popcount class per launch)
+bool use_class_path(int backend) { return backend == 0 || backend == 1; }
 
 // Upload the tables and launch every nonempty class (largest classes first).
-int enqueue_classes(int arith, const cd* at, const cd* dg, int n_half, const std::vector<Seg>& segs,
+int enqueue_classes(int backend, int arith, const cd* at, const cd* dg, int n_half, const std::vector<Seg>& segs,
                     int batch, long long term_stride, long long at_stride, long long dg_stride,
                     int loops, int cap, cd* terms, int8_t* status, void* table_ws,
                     cudaStream_t st) {
@@ -323,7 +335,8 @@ int enqueue_classes(int arith, const cd* at, const cd* dg, int n_half, const std
         ci.term_stride = term_stride;
         ci.at_stride = at_stride;
         ci.dg_stride = dg_stride;
-        cudaError_t e = launch_class(arith, loops, 2 * m, at, dg, n_half, ci, cap, terms, status, st);
+        cudaError_t e = launch_class(backend, arith, loops, 2 * m, at, dg, n_half, ci, cap, terms,
+                                     status, st);
         ++g_launches;
         if (e != cudaSuccess) return cuda_fail("fast class launch", e);
     }
@@ -360,7 +373,7 @@ int enqueue_mask_range(const cd* at, const cd* dg, int n_half, uint64_t lo, uint
             segs[0].hi = hi;
             segs[0].out_off = 0;
             void* tw = static_cast<char*>(ws) + terms_ws_bytes(count);
-            int rc = enqueue_classes(arith, at, dg, n_half, segs, 1, 0, 0, 0, loops, cap, terms,
+            int rc = enqueue_classes(backend, arith, at, dg, n_half, segs, 1, 0, 0, 0, loops, cap, terms,
                                      status, tw, st);
             if (rc) return rc;
         } else {
@@ -402,7 +415,7 @@ int enqueue_range_list(const cd* at, const cd* dg, int n_half, int n_ranges, con
                 segs[p].hi = std::min(a + width, total);
                 segs[p].out_off = (long long)p * (long long)width;
             }
-            int rc = enqueue_classes(arith, at, dg, n_half, segs, 1, 0, 0, 0, loops, cap, terms,
+            int rc = enqueue_classes(backend, arith, at, dg, n_half, segs, 1, 0, 0, 0, loops, cap, terms,
                                      status, tw, st);
             if (rc) return rc;
         } else {
@@ -643,7 +656,7 @@ int hafb_sum_subsets_fast(const double* atilde, const double* diag, int n_half, 
         segs[0].lo = 1;
         segs[0].hi = total;
         segs[0].out_off = 0;
-        rc = enqueue_classes(arith, d_at, d_dg, n_half, segs, 1, 0, 0, 0, include_loops, cap_mult,
+        rc = enqueue_classes(backend, arith, d_at, d_dg, n_half, segs, 1, 0, 0, 0, include_loops, cap_mult,
                                   terms, status, static_cast<char*>(d_ws) + terms_ws_bytes(count),
                                   c.st);
         if (rc) return rc;
@@ -718,8 +731,8 @@ int hafb_terms(const double* atilde, const double* diag, int n_half, const uint6
             ci.n_items = per;
             ci.mlist = d_sm + start[m];
             ci.mout = d_so + start[m];
-            cudaError_t e = launch_class(arith, include_loops, 2 * m, d_at, d_dg, n_half, ci,
-                                         cap_mult, d_t, d_s, c.st);
+            cudaError_t e = launch_class(backend, arith, include_loops, 2 * m, d_at, d_dg, n_half,
+                                         ci, cap_mult, d_t, d_s, c.st);
             if (e != cudaSuccess) return cuda_fail("fast class launch", e);
             ++g_launches;
         }
@@ -771,7 +784,7 @@ int hafb_batch(const double* atilde, const double* diag, int batch, int n_half, 
         segs[0].lo = 1;
         segs[0].hi = total;
         segs[0].out_off = 0;
-        rc = enqueue_classes(arith, d_at, d_dg, n_half, segs, batch, per, (long long)n * n, n,
+        rc = enqueue_classes(backend, arith, d_at, d_dg, n_half, segs, batch, per, (long long)n * n, n,
                                   include_loops, cap_mult, d_t, d_s, d_tab, c.st);
         if (rc) return rc;
     } else {

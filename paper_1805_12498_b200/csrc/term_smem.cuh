@@ -26,17 +26,20 @@ namespace hafb {
 constexpr int kMaxHalf = 31;  // masks are 32-bit on the device; s <= 62
 constexpr double kDeflationRtol = 1e-14;  // _numba.py:32
 
-// shared-memory footprint (in cd elements) of one warp's workspace for size n
-__host__ __device__ inline int smem_warp_elems(int n) {
-    int K = n / 2;
-    int pt = (n + 1) * (n + 2) / 2;  // triangular charpoly table
-    return n * n + pt + 6 * (n + 2) + 3 * (K + 2);
+// shared-memory footprint (in cd elements) of one warp's workspace for subset
+// matrices up to size S with K = n/2 power traces (S = n when the warp may see any
+// subset; S = 2m for a one-class launch)
+__host__ __device__ inline int smem_warp_elems(int S, int K) {
+    int hreg = S * S > S * K ? S * S : S * K;  // H doubles as the power-sum scratch
+    int pt = (S + 1) * (S + 2) / 2;            // triangular charpoly table
+    return hreg + pt + 6 * (S + 2) + 3 * (K + 2);
 }
+__host__ __device__ inline int smem_warp_elems(int n) { return smem_warp_elems(n, n / 2); }
 
 struct WarpWs {
-    cd* H;    // s*s, row-major, ld = s
+    cd* H;    // s*s, row-major, ld = s (also the s*K power-sum scratch)
     cd* P;    // triangular: row k at k(k+1)/2, length k+1
-    cd* vec;  // misc vectors, each n+2
+    cd* vec;  // misc vectors, each S+2
     cd* mu;
     cd* v;
     cd* xv;
@@ -48,24 +51,25 @@ struct WarpWs {
     cd* E;    // K+2
 };
 
-__device__ inline WarpWs carve(cd* base, int n) {
+__device__ inline WarpWs carve(cd* base, int S, int K) {
     WarpWs w;
-    int K = n / 2;
+    int hreg = S * S > S * K ? S * S : S * K;
     w.H = base;
-    w.P = w.H + n * n;
-    cd* q = w.P + (n + 1) * (n + 2) / 2;
-    w.mu = q; q += n + 2;
-    w.v = q; q += n + 2;
-    w.xv = q; q += n + 2;
-    w.u = q; q += n + 2;
-    w.unew = q; q += n + 2;
-    w.eig = q; q += n + 2;
+    w.P = w.H + hreg;
+    cd* q = w.P + (S + 1) * (S + 2) / 2;
+    w.mu = q; q += S + 2;
+    w.v = q; q += S + 2;
+    w.xv = q; q += S + 2;
+    w.u = q; q += S + 2;
+    w.unew = q; q += S + 2;
+    w.eig = q; q += S + 2;
     w.t = q; q += K + 2;
     w.s = q; q += K + 2;
     w.E = q; q += K + 2;
     w.vec = nullptr;
     return w;
 }
+__device__ inline WarpWs carve(cd* base, int n) { return carve(base, n, n / 2); }
 
 // ------------------------------------------------------------------ Hessenberg
 // _numba.py:36-67.  The i-loop is sequential (each i's row op then column op);
@@ -479,8 +483,8 @@ __global__ void __launch_bounds__(256) terms_smem_class_kernel(
     extern __shared__ cd smem[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
-    const int n = 2 * n_half;
-    WarpWs w = carve(smem + (size_t)wib * smem_warp_elems(n), n);
+    const int S = 2 * ci.m;  // one class per launch: size the workspace for it
+    WarpWs w = carve(smem + (size_t)wib * smem_warp_elems(S, n_half), S, n_half);
     const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
     for (long long it = (long long)blockIdx.x * (blockDim.x >> 5) + wib; it < ci.n_items; it += nwarps) {
         const ItemRef ir = resolve_item(ci, it);

@@ -21,7 +21,7 @@ static cudaError_t launch_one(const cd* at, const cd* dg, int n_half, const Clas
     constexpr int W = TeamWidth<S>::W;
     constexpr int TPB = kFastThreads / W;
     constexpr bool SH = smem_hess(S);
-    const size_t smem = (size_t)TPB * FastLayout<S, SH>::TOTAL * sizeof(cd) + (kDMax + 1) * sizeof(double);
+    const size_t smem = (size_t)TPB * FastLayout<S, SH, L>::TOTAL * sizeof(cd) + (kDMax + 1) * sizeof(double);
     auto kern = fast_term_kernel<S, L, SH>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -80,18 +80,18 @@ constexpr int kDMax = 31;
 // and starts at c(c+3)/2.
 __host__ __device__ constexpr int hs_elems(int S) { return (S - 1) * (S + 2) / 2 + S; }
 
-template <int S, bool SH = false>
+template <int S, bool SH = false, bool LOOPS = true>
 struct FastLayout {
     static constexpr int HS = 0;                      // packed Hessenberg, or (SH) the S x S matrix
     static constexpr int SP = S + 12;                  // padded pivot-row / multiplier length
-    static constexpr int PR = HS + (SH ? S * S : hs_elems(S));  // [2][SP] pivot rows
-    static constexpr int MU = PR + 2 * SP;            // [2][SP] multipliers
+    static constexpr int PR = HS + (SH ? S * S : hs_elems(S));  // [2][SP] pivot rows (register variant)
+    static constexpr int MU = PR + (SH ? 0 : 2 * SP);  // [2][SP] multipliers
     static constexpr int CF = MU + 2 * SP;            // [2][S] charpoly coefs
     static constexpr int RED = CF + 2 * S;            // [2][2][2] argmax exchange (W = 64)
     static constexpr int A = RED + 8;                 // [S+1] charpoly coefficients
-    static constexpr int U = A + S + 1;               // [2][S] loop-chain vector
-    static constexpr int PX = U + 2 * S;              // [S] charpoly cross-warp exchange
-    static constexpr int T = PX + S;                  // [kDMax+2] traces / exp broadcast
+    static constexpr int U = A + S + 1;               // [2][S] loop-chain vector (LOOPS)
+    static constexpr int PX = U + (LOOPS ? 2 * S : 0);  // [S] cross-warp exchange (W = 64)
+    static constexpr int T = PX + (S > 32 ? S : 4);   // [kDMax+2] traces / exp broadcast
     static constexpr int G = T + kDMax + 2;           // [kDMax+2] g_j = j s_j
     static constexpr int FLAG = G + kDMax + 2;        // [1]
     static constexpr int SIGN = (S + 3) / 4 + 1;      // cd slots holding S ints
@@ -382,9 +382,9 @@ __device__ __forceinline__ void fast_hessenberg(cd (&w)[S], int& myrow, const Te
 // occupancy hides the per-step serial latency).  Rows are relabelled (lane <->
 // logical row); `lm` (logical row -> lane, double-buffered) is kept for the
 // charpoly.  Same arithmetic identities as fast_hessenberg.
-template <int S, int W>
+template <int S, int W, bool LOOPS>
 __device__ __forceinline__ void smem_hessenberg(cd* H, int& myrow, const TeamCtx<W>& tc, cd* ws) {
-    using L = FastLayout<S, true>;
+    using L = FastLayout<S, true, LOOPS>;
     const int lane = tc.lane;
     int* lm0 = reinterpret_cast<int*>(ws + L::SIG);
     if (lane < S) lm0[lane] = lane;
@@ -395,10 +395,12 @@ __device__ __forceinline__ void smem_hessenberg(cd* H, int& myrow, const TeamCtx
         const int B = J & 1;
         const int* lm = reinterpret_cast<const int*>(ws + L::SIG + B * L::SIGN);
         int* lm_next = reinterpret_cast<int*>(ws + L::SIG + (1 - B) * L::SIGN);
+        HT_DECL
         const cd x = lane < S ? H[J * S + lane] : mk(0.0, 0.0);
         const double key = (myrow > J && myrow < S) ? fabs(x.re) + fabs(x.im) : 0.0;
         unsigned kbits;
         const int wl = team_argmax_lane<W>(tc, ws + L::RED + 4 * B, key, kbits);
+        HT_MARK(8);
         if (kbits == 0u) {  // nothing to eliminate below the subdiagonal
             if (lane < S) lm_next[lane] = lm[lane];
             tc.sync();
@@ -432,6 +434,7 @@ __device__ __forceinline__ void smem_hessenberg(cd* H, int& myrow, const TeamCtx
             if constexpr (W > 32) H[(J + 1) * S + lane] = xb;  // read back as pv1 below
             x1 = xb;
         }
+        HT_MARK(9);
         const cd ip = f_inv(p);
         const bool elim = myrow >= J + 2 && myrow < S;
         const cd mu = elim ? f_mul(x, ip) : mk(0.0, 0.0);
@@ -444,6 +447,7 @@ __device__ __forceinline__ void smem_hessenberg(cd* H, int& myrow, const TeamCtx
         }
         tc.sync();
         if constexpr (W > 32) pv1 = H[(J + 1) * S + wl];  // read before column J+1 changes
+        HT_MARK(10);
         const cd hj1 = f_cms(x1, mu, pv1);
         cd acc0 = mk(0.0, 0.0), acc1 = mk(0.0, 0.0);
         const cd* prow = H + wl;  // the pivot row, read in place
@@ -469,6 +473,7 @@ __device__ __forceinline__ void smem_hessenberg(cd* H, int& myrow, const TeamCtx
         }
         if constexpr (W > 32) tc.sync();  // everyone has read pv1 before column J+1 changes
         if (lane < S) H[(J + 1) * S + lane] = f_add(hj1, f_add(acc0, acc1));
+        HT_MARK(11);
     }
     tc.sync();
 }
@@ -483,7 +488,7 @@ __global__ void __launch_bounds__(kFastThreads) fast_term_kernel(const cd* __res
     constexpr int TPB = kFastThreads / W;
     constexpr int M = S / 2;
     constexpr int R = (kDMax + W - 1) / W;  // coefficient chunks per lane
-    using L = FastLayout<S, SH>;
+    using L = FastLayout<S, SH, LOOPS>;
     extern __shared__ cd smem[];
     TeamCtx<W> tc;
     tc.tib = threadIdx.x / W;
@@ -583,7 +588,7 @@ __global__ void __launch_bounds__(kFastThreads) fast_term_kernel(const cd* __res
             });
             tc.sync();
             HT_MARK(0);
-            smem_hessenberg<S, W>(H, myrow, tc, ws);
+            smem_hessenberg<S, W, LOOPS>(H, myrow, tc, ws);
         } else {
             static_for<0, S>([&](auto c) {
                 const int vc = 2 * vbit[c() >> 1] + (c() & 1);

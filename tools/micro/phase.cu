@@ -37,7 +37,7 @@ int main(int argc, char** argv) {
 #ifndef SHV
 #define SHV true
 #endif
-    size_t smem = (size_t)TPB * FastLayout<HAFB_S, SHV>::TOTAL * sizeof(cd) + (kDMax + 1) * 8;
+    size_t smem = (size_t)TPB * FastLayout<HAFB_S, SHV, false>::TOTAL * sizeof(cd) + (kDMax + 1) * 8;
     auto k = fast_term_kernel<HAFB_S, false, SHV>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int occ; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kFastThreads, smem);
@@ -58,7 +58,7 @@ int main(int argc, char** argv) {
     cudaMemcpyFromSymbol(ph, g_phase, sizeof(ph)); cudaMemcpyFromSymbol(pc, g_phase_cnt, sizeof(pc));
 #endif
     printf("S=%d items=%lld grid=%d occ=%d time=%.3f ms err=%s\n", HAFB_S, prefix[1], grid, occ, ms, cudaGetErrorString(cudaGetLastError()));
-    const char* names[16] = {"enum+gather", "hessenberg", "charpoly", "newton", "exp+store", "h:shfl", "h:relabel+Hs", "h:inv+mu", "h:argmax", "h:swap", "h:publish+sync", "h:sweep", "h:shift", "EMPTY(mark cost)"};
+    const char* names[16] = {"enum+gather", "hessenberg", "charpoly", "newton", "exp+store", "h:shfl", "h:relabel+Hs", "h:inv+mu", "h:argmax", "h:shfl+lm+swap", "h:inv+mu+sync", "h:sweep", "h:shift", "EMPTY(mark cost)"};
     unsigned long long items = pc[0];
     for (int i = 0; i < 14; ++i) if (pc[i]) printf("  %-20s %10.0f cycles/item  (%llu marks)\n", names[i], (double)ph[i] / items, pc[i]);
     return 0;

@@ -35,3 +35,16 @@ for name, A, loops, lohi in cases:
               f"fails={int(f.max())} result={r}", flush=True)
     if "mirror" in res:
         print(f"   rel diff fast vs mirror: {abs(res['fast']-res['mirror'])/abs(res['mirror']):.3e}")
+
+if len(sys.argv) > 1 and sys.argv[-1] in ("batch", "full"):
+    # cfg1: batch of 4096 GBS-like hafnians, n = 24
+    mats = [W.cfg1(s) for s in range(4096)]
+    for arith in ("fast", "mirror"):
+        for rep in range(2):
+            t = time.perf_counter()
+            res = engine.hafnian_batch(mats, backend="charpoly", arith=arith)
+            dt = time.perf_counter() - t
+        nt = 4096 * 4095
+        fl = 4096 * costmodel.flops_total(12)
+        print(f"cfg1 batch {arith:6s} {dt*1e3:9.2f} ms  {nt/dt:.3e} terms/s  {fl/dt/1e12:.3f} TF/s  "
+              f"res[0]={res[0]}", flush=True)

@@ -126,6 +126,20 @@ int hafb_sum_range_list_async(const double* d_atilde, const double* d_diag, int 
                               size_t workspace_bytes, double* d_partials, int64_t* d_fails,
                               void* stream, void* terms_done_event);
 
+/* Exact mode for INTEGER matrices (no reference counterpart:
+ * the reference returns a float, inexact beyond 2^53, e.g. cfg3).  The subset sum
+ * of engine.py:153-178 evaluated in GF(p) for each prime: per subset the same
+ * Hessenberg / charpoly / Newton / exp-coefficient steps as _numba.py:36-351 with
+ * field arithmetic (first-nonzero pivot, divisions by k and 2k as inverses mod p).
+ * atilde_p: n_primes x n x n residues of the prepared X.A (row-major, the same
+ * preparation as `atilde`); diag_p: n_primes x n residues of the loop weights;
+ * primes: odd, n < p < 2^31; masks [lo, hi) of the 2^n_half subsets (mask 0 adds 0).
+ * residues[i] = (sum of the signed terms) mod primes[i]; the host lifts them to the
+ * exact integer by CRT.  device_ms (nullable) = device time of the term kernels. */
+int hafb_modp_sums(const uint32_t* atilde_p, const uint32_t* diag_p, const uint32_t* primes,
+                   int n_primes, int n_half, uint64_t lo, uint64_t hi, int include_loops,
+                   int device, uint64_t* residues, double* device_ms);
+
 /* Calibration: FP64 FMA throughput of `device` measured by a DFMA-saturating probe
  * kernel (the roofline denominator for the subset-term kernels).  tflops = 2 flop/DFMA. */
 int hafb_fp64_peak(int device, double* tflops, double* ms);

@@ -113,3 +113,31 @@ def bipartite_embedding(W) -> np.ndarray:
     out[:m, m:] = w
     out[m:, :m] = w.T
     return out
+
+
+def hafnian_exact_dp(A, loops: bool = False) -> int:
+    """Exact (loop) hafnian of an integer matrix with Python ints: the lowest
+    remaining vertex is matched to each other remaining vertex (or, with loops,
+    to itself), memoised over the remaining-vertex bitmask.  O(2^n n); n <= 20.
+    Independent of the subset-sum formula (checks the exact GF(p) mode)."""
+    rows = [[int(v) for v in r] for r in np.asarray(A, dtype=object).tolist()] if len(A) else []
+    n = len(rows)
+
+    @lru_cache(maxsize=None)
+    def rec(rem: int) -> int:
+        if rem == 0:
+            return 1
+        i = (rem & -rem).bit_length() - 1
+        rest = rem & ~(1 << i)
+        total = rows[i][i] * rec(rest) if loops else 0
+        r = rest
+        while r:
+            j = (r & -r).bit_length() - 1
+            r &= r - 1
+            if rows[i][j]:
+                total += rows[i][j] * rec(rest & ~(1 << j))
+        return total
+
+    if n % 2 and not loops:
+        return 0
+    return rec((1 << n) - 1)

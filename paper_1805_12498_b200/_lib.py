@@ -26,6 +26,7 @@ _dp = ctypes.POINTER(ctypes.c_double)
 _i64p = ctypes.POINTER(ctypes.c_int64)
 _i32p = ctypes.POINTER(ctypes.c_int32)
 _u64p = ctypes.POINTER(ctypes.c_uint64)
+_u32p = ctypes.POINTER(ctypes.c_uint32)
 _vp = ctypes.c_void_p
 _int, _u64, _i64, _size = ctypes.c_int, ctypes.c_uint64, ctypes.c_int64, ctypes.c_size_t
 
@@ -53,6 +54,7 @@ SIGNATURES = {
                                          _int, _vp, _size, _vp, _vp, _vp, _vp]),
     "hafb_launch_count": (_i64, [_int]),
     "hafb_fp64_peak": (_int, [_int, _dp, _dp]),
+    "hafb_modp_sums": (_int, [_u32p, _u32p, _u32p, _int, _int, _u64, _u64, _int, _int, _u64p, _dp]),
 }
 
 

@@ -3,7 +3,8 @@
     python -m paper_1805_12498_b200.build [--force] [-v]
 
 Compiles csrc/hafb200.cu (ABI, shared-memory kernels, reductions) and one
-object per register-kernel size (csrc/fast_inst.cu with -DHAFB_S=S) in
+object per register-kernel size (csrc/fast_inst.cu, mirror_inst.cu, modp_inst.cu
+with -DHAFB_S=S) in
 parallel, then links ``paper_1805_12498_b200/libhafb200.so``.  The .so is
 git-ignored but travels to the GPU box with the repo snapshot.
 """
@@ -62,6 +63,8 @@ def _units():
         units.append((f"fast_{s:02d}.o", os.path.join(CSRC, "fast_inst.cu"), [f"-DHAFB_S={s}"]))
     for s in MIRROR_SIZES:
         units.append((f"mirror_{s:02d}.o", os.path.join(CSRC, "mirror_inst.cu"), [f"-DHAFB_S={s}"]))
+    for s in MIRROR_SIZES:
+        units.append((f"modp_{s:02d}.o", os.path.join(CSRC, "modp_inst.cu"), [f"-DHAFB_S={s}"]))
     return units
 
 

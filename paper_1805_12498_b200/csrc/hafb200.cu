@@ -295,52 +295,90 @@ cudaError_t launch_class(int backend, int arith, bool loops, int S, const cd* at
 // every backend runs on the class path (one popcount class per launch)
 bool use_class_path(int backend) { return backend == 0 || backend == 1; }
 
+// Device copies of the class-enumeration tables (carved from `table_ws`).
+struct DevTables {
+    ClassTables t;
+    unsigned long long* binom = nullptr;
+    Seg* segs = nullptr;
+    long long* prefix = nullptr;
+    unsigned long long* base = nullptr;
+    // the items of popcount class m (batch problems of `per` items each)
+    ClassItems items(int m, int batch, long long term_stride, long long at_stride,
+                     long long dg_stride) const {
+        const size_t nseg = (size_t)t.nseg;
+        ClassItems ci;
+        ci.mlist = nullptr;
+        ci.mout = nullptr;
+        ci.binom = binom;
+        ci.segs = segs;
+        ci.prefix = prefix + (size_t)m * (nseg + 1);
+        ci.base = base + (size_t)m * nseg;
+        ci.nseg = (int)nseg;
+        ci.m = m;
+        ci.D = t.D;
+        ci.per_problem = t.count(m);
+        ci.n_items = ci.per_problem * batch;
+        ci.term_stride = term_stride;
+        ci.at_stride = at_stride;
+        ci.dg_stride = dg_stride;
+        return ci;
+    }
+};
+
+int upload_tables(int D, const std::vector<Seg>& segs, void* table_ws, cudaStream_t st, DevTables& dt) {
+    dt.t = build_tables(D, segs);
+    const size_t nseg = segs.size();
+    char* p = static_cast<char*>(table_ws);
+    dt.binom = reinterpret_cast<unsigned long long*>(p);
+    p += align256(sizeof(g_binom_host));
+    dt.segs = reinterpret_cast<Seg*>(p);
+    p += align256(sizeof(Seg) * nseg);
+    dt.prefix = reinterpret_cast<long long*>(p);
+    p += align256(sizeof(long long) * dt.t.prefix.size());
+    dt.base = reinterpret_cast<unsigned long long*>(p);
+    CK(cudaMemcpyAsync(dt.binom, g_binom_host, sizeof(g_binom_host), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dt.segs, segs.data(), sizeof(Seg) * nseg, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dt.prefix, dt.t.prefix.data(), sizeof(long long) * dt.t.prefix.size(),
+                       cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dt.base, dt.t.base.data(), sizeof(unsigned long long) * dt.t.base.size(),
+                       cudaMemcpyHostToDevice, st));
+    return HAFB_OK;
+}
+
 // Upload the tables and launch every nonempty class (largest classes first).
 int enqueue_classes(int backend, int arith, const cd* at, const cd* dg, int n_half, const std::vector<Seg>& segs,
                     int batch, long long term_stride, long long at_stride, long long dg_stride,
                     int loops, int cap, cd* terms, int8_t* status, void* table_ws,
                     cudaStream_t st) {
     const int D = n_half;
-    ClassTables t = build_tables(D, segs);
-    const size_t nseg = segs.size();
-    char* p = static_cast<char*>(table_ws);
-    unsigned long long* d_binom = reinterpret_cast<unsigned long long*>(p);
-    p += align256(sizeof(g_binom_host));
-    Seg* d_segs = reinterpret_cast<Seg*>(p);
-    p += align256(sizeof(Seg) * nseg);
-    long long* d_prefix = reinterpret_cast<long long*>(p);
-    p += align256(sizeof(long long) * t.prefix.size());
-    unsigned long long* d_base = reinterpret_cast<unsigned long long*>(p);
-    CK(cudaMemcpyAsync(d_binom, g_binom_host, sizeof(g_binom_host), cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(d_segs, segs.data(), sizeof(Seg) * nseg, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(d_prefix, t.prefix.data(), sizeof(long long) * t.prefix.size(),
-                       cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(d_base, t.base.data(), sizeof(unsigned long long) * t.base.size(),
-                       cudaMemcpyHostToDevice, st));
+    DevTables dt;
+    int rc = upload_tables(D, segs, table_ws, st, dt);
+    if (rc) return rc;
     for (int m = D; m >= 1; --m) {
-        long long per = t.count(m);
-        if (per == 0) continue;
-        ClassItems ci;
-        ci.mlist = nullptr;
-        ci.mout = nullptr;
-        ci.binom = d_binom;
-        ci.segs = d_segs;
-        ci.prefix = d_prefix + (size_t)m * (nseg + 1);
-        ci.base = d_base + (size_t)m * nseg;
-        ci.nseg = (int)nseg;
-        ci.m = m;
-        ci.D = D;
-        ci.per_problem = per;
-        ci.n_items = per * batch;
-        ci.term_stride = term_stride;
-        ci.at_stride = at_stride;
-        ci.dg_stride = dg_stride;
+        if (dt.t.count(m) == 0) continue;
+        const ClassItems ci = dt.items(m, batch, term_stride, at_stride, dg_stride);
         cudaError_t e = launch_class(backend, arith, loops, 2 * m, at, dg, n_half, ci, cap, terms,
                                      status, st);
         ++g_launches;
         if (e != cudaSuccess) return cuda_fail("fast class launch", e);
     }
     return HAFB_OK;
+}
+
+cudaError_t launch_modp_class(int S, bool loops, const uint32_t* at, const uint32_t* dg, int n_half,
+                              const ClassItems& ci, uint32_t p, const uint32_t* inv,
+                              unsigned long long* total, cudaStream_t st) {
+    const int sms = sm_count();
+    switch (S) {
+#define PC(SS) \
+    case SS: return launch_modp_S<SS>(loops, at, dg, n_half, ci, p, inv, total, st, sms);
+        PC(2) PC(4) PC(6) PC(8) PC(10) PC(12) PC(14) PC(16) PC(18) PC(20) PC(22) PC(24)
+        PC(26) PC(28) PC(30) PC(32) PC(34) PC(36) PC(38) PC(40) PC(42) PC(44) PC(46) PC(48)
+        PC(50) PC(52) PC(54) PC(56) PC(58) PC(60) PC(62)
+#undef PC
+        default:
+            return cudaErrorInvalidValue;
+    }
 }
 
 size_t table_ws_bytes(int n_half, size_t nseg) {
@@ -862,6 +900,86 @@ int hafb_charpoly_coefficients(const double* b, int m, int arith, int device, do
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(coeffs, d_o, sizeof(cd) * (m + 1), cudaMemcpyDeviceToHost, c.st));
     CK(cudaStreamSynchronize(c.st));
+    return HAFB_OK;
+}
+
+int hafb_modp_sums(const uint32_t* atilde_p, const uint32_t* diag_p, const uint32_t* primes,
+                   int n_primes, int n_half, uint64_t lo, uint64_t hi, int include_loops,
+                   int device, uint64_t* residues, double* device_ms) {
+    g_err.clear();
+    if (n_half < 1 || n_half > kMaxHalf) return fail(HAFB_ERR_ARG, "n_half must be in [1, 31]");
+    if (n_primes < 1 || n_primes > 64) return fail(HAFB_ERR_ARG, "n_primes must be in [1, 64]");
+    if (hi < lo || hi > (1ull << n_half)) return fail(HAFB_ERR_ARG, "bad mask range");
+    const int n = 2 * n_half;
+    for (int i = 0; i < n_primes; ++i)
+        if (primes[i] <= (uint32_t)n || primes[i] >= (1u << 31) || (primes[i] & 1u) == 0)
+            return fail(HAFB_ERR_ARG, "primes must be odd, > n and < 2^31");
+    constexpr int KI = kMaxHalf + 1;  // inverses of 1..D (kDMax + 1 in term_modp.cuh)
+    std::vector<uint32_t> inv((size_t)n_primes * KI, 0u);
+    for (int i = 0; i < n_primes; ++i) {
+        const uint64_t p = primes[i];
+        for (int k = 1; k < KI; ++k) {  // k^(p-2) mod p (Fermat)
+            uint64_t r = 1, a = (uint64_t)k, e = p - 2;
+            while (e) {
+                if (e & 1) r = r * a % p;
+                a = a * a % p;
+                e >>= 1;
+            }
+            inv[(size_t)i * KI + k] = (uint32_t)r;
+        }
+    }
+    Call c;
+    uint32_t *d_at, *d_dg, *d_inv;
+    unsigned long long* d_tot;
+    void* d_tab;
+    std::vector<Seg> segs(1);
+    segs[0].lo = lo;
+    segs[0].hi = hi;
+    segs[0].out_off = 0;
+    CK(c.open(device));
+    CK(c.alloc(&d_at, sizeof(uint32_t) * n_primes * n * n));
+    CK(c.alloc(&d_dg, sizeof(uint32_t) * n_primes * n));
+    CK(c.alloc(&d_inv, sizeof(uint32_t) * inv.size()));
+    CK(c.alloc(&d_tot, sizeof(unsigned long long) * n_primes));
+    CK(c.alloc(&d_tab, table_ws_bytes(n_half, 1)));
+    CK(cudaMemcpyAsync(d_at, atilde_p, sizeof(uint32_t) * n_primes * n * n, cudaMemcpyHostToDevice, c.st));
+    CK(cudaMemcpyAsync(d_dg, diag_p, sizeof(uint32_t) * n_primes * n, cudaMemcpyHostToDevice, c.st));
+    CK(cudaMemcpyAsync(d_inv, inv.data(), sizeof(uint32_t) * inv.size(), cudaMemcpyHostToDevice, c.st));
+    CK(cudaMemsetAsync(d_tot, 0, sizeof(unsigned long long) * n_primes, c.st));
+    DevTables dt;
+    int rc = upload_tables(n_half, segs, d_tab, c.st, dt);
+    if (rc) return rc;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (device_ms) {
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0, c.st));
+    }
+    for (int i = 0; i < n_primes; ++i) {
+        for (int m = n_half; m >= 1; --m) {
+            if (dt.t.count(m) == 0) continue;
+            const ClassItems ci = dt.items(m, 1, 0, 0, 0);
+            cudaError_t e = launch_modp_class(2 * m, include_loops != 0, d_at + (size_t)i * n * n,
+                                              d_dg + (size_t)i * n, n_half, ci, primes[i],
+                                              d_inv + (size_t)i * KI, d_tot + i, c.st);
+            ++g_launches;
+            if (e != cudaSuccess) return cuda_fail("modp class launch", e);
+        }
+    }
+    if (device_ms) {
+        CK(cudaEventRecord(e1, c.st));
+    }
+    std::vector<unsigned long long> tot(n_primes);
+    CK(cudaMemcpyAsync(tot.data(), d_tot, sizeof(unsigned long long) * n_primes, cudaMemcpyDeviceToHost, c.st));
+    CK(cudaStreamSynchronize(c.st));
+    if (device_ms) {
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, e0, e1));
+        *device_ms = t;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    }
+    for (int i = 0; i < n_primes; ++i) residues[i] = tot[i] % primes[i];
     return HAFB_OK;
 }
 

@@ -14,6 +14,7 @@ results; "fast": FMA-contracted kernels) and ``device`` (CUDA ordinal).
 
 from __future__ import annotations
 
+import ctypes
 import os
 
 import numpy as np
@@ -178,3 +179,24 @@ def charpoly_coefficients(b, *, device=None):
     _lib.check(lib.hafb_charpoly_coefficients(_lib.dptr(h), h.shape[0], 0, _device(device),
                                               _lib.dptr(out)))
     return out
+
+
+def modp_sums(atilde_p, diag_p, primes, n_half, lo, hi, include_loops, *, device=None):
+    """Exact-mode residues: the signed subset sum over masks [lo, hi) modulo each
+    prime (hafb_modp_sums).  atilde_p / diag_p: residues, one slice per prime.
+    Returns (uint64[n_primes] residues, device milliseconds of the term kernels)."""
+    lib = _lib.load(require_device=True)
+    pr = np.ascontiguousarray(primes, dtype=np.uint32)
+    at = np.ascontiguousarray(atilde_p, dtype=np.uint32)
+    dg = np.ascontiguousarray(diag_p, dtype=np.uint32)
+    n = 2 * int(n_half)
+    if at.size != pr.size * n * n or dg.size != pr.size * n:
+        raise ValueError("residue arrays do not match n_primes x n x n / n_primes x n")
+    res = np.zeros(pr.size, np.uint64)
+    ms = ctypes.c_double(0.0)
+    u32 = ctypes.POINTER(ctypes.c_uint32)
+    _lib.check(lib.hafb_modp_sums(at.ctypes.data_as(u32), dg.ctypes.data_as(u32),
+                                  pr.ctypes.data_as(u32), int(pr.size), int(n_half), int(lo),
+                                  int(hi), int(bool(include_loops)), _device(device),
+                                  _lib.u64ptr(res), ctypes.byref(ms)))
+    return res, ms.value

@@ -18,6 +18,7 @@
 #include "reduce.cuh"
 #include "term_smem.cuh"
 #include "fast_launch.h"
+#include "term_modp.cuh"
 
 using namespace hafb;
 
@@ -914,22 +915,27 @@ int hafb_modp_sums(const uint32_t* atilde_p, const uint32_t* diag_p, const uint3
     for (int i = 0; i < n_primes; ++i)
         if (primes[i] <= (uint32_t)n || primes[i] >= (1u << 31) || (primes[i] & 1u) == 0)
             return fail(HAFB_ERR_ARG, "primes must be odd, > n and < 2^31");
-    constexpr int KI = kMaxHalf + 1;  // inverses of 1..D (kDMax + 1 in term_modp.cuh)
-    std::vector<uint32_t> inv((size_t)n_primes * KI, 0u);
+    // Montgomery form (x 2^32 mod p) of the inputs and the per-prime constants
+    std::vector<uint32_t> tab((size_t)n_primes * kModpTab, 0u);
+    std::vector<uint32_t> atm((size_t)n_primes * n * n), dgm((size_t)n_primes * n);
     for (int i = 0; i < n_primes; ++i) {
         const uint64_t p = primes[i];
-        for (int k = 1; k < KI; ++k) {  // k^(p-2) mod p (Fermat)
+        auto mont = [p](uint64_t v) { return (uint32_t)(((v % p) << 32) % p); };
+        for (int k = 1; k < kModpTabK; ++k) {  // k^(p-2) mod p (Fermat)
             uint64_t r = 1, a = (uint64_t)k, e = p - 2;
             while (e) {
                 if (e & 1) r = r * a % p;
                 a = a * a % p;
                 e >>= 1;
             }
-            inv[(size_t)i * KI + k] = (uint32_t)r;
+            tab[(size_t)i * kModpTab + k] = mont(r);
+            tab[(size_t)i * kModpTab + kModpTabK + k] = mont((uint64_t)k);
         }
+        for (size_t e = 0; e < (size_t)n * n; ++e) atm[(size_t)i * n * n + e] = mont(atilde_p[(size_t)i * n * n + e]);
+        for (int e = 0; e < n; ++e) dgm[(size_t)i * n + e] = mont(diag_p[(size_t)i * n + e]);
     }
     Call c;
-    uint32_t *d_at, *d_dg, *d_inv;
+    uint32_t *d_at, *d_dg, *d_ktab;
     unsigned long long* d_tot;
     void* d_tab;
     std::vector<Seg> segs(1);
@@ -939,12 +945,12 @@ int hafb_modp_sums(const uint32_t* atilde_p, const uint32_t* diag_p, const uint3
     CK(c.open(device));
     CK(c.alloc(&d_at, sizeof(uint32_t) * n_primes * n * n));
     CK(c.alloc(&d_dg, sizeof(uint32_t) * n_primes * n));
-    CK(c.alloc(&d_inv, sizeof(uint32_t) * inv.size()));
+    CK(c.alloc(&d_ktab, sizeof(uint32_t) * tab.size()));
     CK(c.alloc(&d_tot, sizeof(unsigned long long) * n_primes));
     CK(c.alloc(&d_tab, table_ws_bytes(n_half, 1)));
-    CK(cudaMemcpyAsync(d_at, atilde_p, sizeof(uint32_t) * n_primes * n * n, cudaMemcpyHostToDevice, c.st));
-    CK(cudaMemcpyAsync(d_dg, diag_p, sizeof(uint32_t) * n_primes * n, cudaMemcpyHostToDevice, c.st));
-    CK(cudaMemcpyAsync(d_inv, inv.data(), sizeof(uint32_t) * inv.size(), cudaMemcpyHostToDevice, c.st));
+    CK(cudaMemcpyAsync(d_at, atm.data(), sizeof(uint32_t) * atm.size(), cudaMemcpyHostToDevice, c.st));
+    CK(cudaMemcpyAsync(d_dg, dgm.data(), sizeof(uint32_t) * dgm.size(), cudaMemcpyHostToDevice, c.st));
+    CK(cudaMemcpyAsync(d_ktab, tab.data(), sizeof(uint32_t) * tab.size(), cudaMemcpyHostToDevice, c.st));
     CK(cudaMemsetAsync(d_tot, 0, sizeof(unsigned long long) * n_primes, c.st));
     DevTables dt;
     int rc = upload_tables(n_half, segs, d_tab, c.st, dt);
@@ -961,7 +967,7 @@ int hafb_modp_sums(const uint32_t* atilde_p, const uint32_t* diag_p, const uint3
             const ClassItems ci = dt.items(m, 1, 0, 0, 0);
             cudaError_t e = launch_modp_class(2 * m, include_loops != 0, d_at + (size_t)i * n * n,
                                               d_dg + (size_t)i * n, n_half, ci, primes[i],
-                                              d_inv + (size_t)i * KI, d_tot + i, c.st);
+                                              d_ktab + (size_t)i * kModpTab, d_tot + i, c.st);
             ++g_launches;
             if (e != cudaSuccess) return cuda_fail("modp class launch", e);
         }

@@ -12,7 +12,7 @@ namespace hafb {
 
 template <int S, bool L>
 static cudaError_t launch_one(const uint32_t* at, const uint32_t* dg, int n_half, const ClassItems& ci,
-                              uint32_t p, const uint32_t* inv, unsigned long long* total,
+                              uint32_t p, const uint32_t* tab, unsigned long long* total,
                               cudaStream_t st, int sms) {
     constexpr int W = TeamWidth<S>::W;
     constexpr int TPB = kModpThreads / W;
@@ -23,22 +23,20 @@ static cudaError_t launch_one(const uint32_t* at, const uint32_t* dg, int n_half
     int occ = 1;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kModpThreads, smem);
     if (e != cudaSuccess) return e;
-    ModP M;
-    M.p = p;
-    M.m = ~0ull / p;
+    ModP M = make_modp(p);
     const long long want = (ci.n_items + TPB - 1) / TPB;
     const long long cap_blocks = (long long)sms * std::max(occ, 1);
     const int grid = (int)std::max<long long>(1, std::min(want, cap_blocks));
-    kern<<<grid, kModpThreads, smem, st>>>(at, dg, n_half, ci, M, inv, total);
+    kern<<<grid, kModpThreads, smem, st>>>(at, dg, n_half, ci, M, tab, total);
     return cudaGetLastError();
 }
 
 template <>
 cudaError_t launch_modp_S<HAFB_S>(bool loops, const uint32_t* at, const uint32_t* dg, int n_half,
-                                  const ClassItems& ci, uint32_t p, const uint32_t* inv,
+                                  const ClassItems& ci, uint32_t p, const uint32_t* tab,
                                   unsigned long long* total, cudaStream_t st, int sms) {
-    return loops ? launch_one<HAFB_S, true>(at, dg, n_half, ci, p, inv, total, st, sms)
-                 : launch_one<HAFB_S, false>(at, dg, n_half, ci, p, inv, total, st, sms);
+    return loops ? launch_one<HAFB_S, true>(at, dg, n_half, ci, p, tab, total, st, sms)
+                 : launch_one<HAFB_S, false>(at, dg, n_half, ci, p, tab, total, st, sms);
 }
 
 }  // namespace hafb

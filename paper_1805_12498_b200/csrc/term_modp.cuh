@@ -24,16 +24,27 @@
 
 namespace hafb {
 
+// Montgomery arithmetic modulo an odd p < 2^31 with R = 2^32: residues are kept
+// as x R mod p (the host uploads them in that form), a product is one 32x32->64
+// multiply plus one REDC (two more multiplies), and a sum of two products
+// (< 2 p^2 < p R) needs a single REDC ("lazy" accumulation).
 struct ModP {
     uint32_t p;
-    unsigned long long m;  // floor(2^64 / p) (Barrett)
-    __device__ __forceinline__ uint32_t red(unsigned long long x) const {  // x < 2^62
-        const unsigned long long q = __umul64hi(x, m);
-        unsigned long long r = x - q * p;
-        return (uint32_t)(r >= p ? r - p : r);
+    uint32_t nq;   // -p^-1 mod 2^32
+    uint32_t one;  // R mod p (1 in Montgomery form)
+    // p - 2 = (2^e_ones - 1) 2^e_r + e_low: the inversion exponent's addition chain
+    int e_ones, e_r;
+    uint32_t e_low;
+    __device__ __forceinline__ uint32_t redc(unsigned long long t) const {  // t < p R
+        const uint32_t m = (uint32_t)t * nq;
+        const uint32_t u = (uint32_t)((t + (unsigned long long)m * p) >> 32);  // < 2p
+        return u >= p ? u - p : u;
     }
     __device__ __forceinline__ uint32_t mul(uint32_t a, uint32_t b) const {
-        return red((unsigned long long)a * b);
+        return redc((unsigned long long)a * b);
+    }
+    __device__ __forceinline__ uint32_t mul2(uint32_t a0, uint32_t b0, uint32_t a1, uint32_t b1) const {
+        return redc((unsigned long long)a0 * b0 + (unsigned long long)a1 * b1);
     }
     __device__ __forceinline__ uint32_t add(uint32_t a, uint32_t b) const {
         const uint32_t s = a + b;
@@ -42,16 +53,51 @@ struct ModP {
     __device__ __forceinline__ uint32_t sub(uint32_t a, uint32_t b) const {
         return a >= b ? a - b : a + p - b;
     }
-    __device__ __forceinline__ uint32_t pow(uint32_t a, uint32_t e) const {
-        uint32_t r = 1;
-        while (e) {
-            if (e & 1u) r = mul(r, a);
-            a = mul(a, a);
-            e >>= 1;
+    // x^-1 = x^(p-2) (Fermat): x^(2^t - 1) by the doubling chain on the bits of t,
+    // then the low bits; ~31 squarings + ~10 multiplies for the primes near 2^31
+    __device__ __forceinline__ uint32_t inv(uint32_t x) const {
+        uint32_t a = x;
+        int s = 1;
+        const int top = 31 - __clz(e_ones);
+        for (int bit = top - 1; bit >= 0; --bit) {
+            uint32_t b = a;
+            for (int i = 0; i < s; ++i) b = mul(b, b);
+            a = mul(b, a);
+            s *= 2;
+            if ((e_ones >> bit) & 1) {
+                a = mul(mul(a, a), x);
+                s += 1;
+            }
         }
-        return r;
+        for (int i = e_r - 1; i >= 0; --i) {
+            a = mul(a, a);
+            if ((e_low >> i) & 1u) a = mul(a, x);
+        }
+        return a;
     }
 };
+
+inline ModP make_modp(uint32_t p) {
+    ModP M;
+    M.p = p;
+    uint32_t x = p;  // p^-1 mod 2^32 by Newton (p p = 1 mod 8 seeds 3 bits)
+    for (int i = 0; i < 5; ++i) x *= 2u - p * x;
+    M.nq = 0u - x;
+    M.one = (uint32_t)((1ull << 32) % p);
+    const uint32_t e = p - 2;
+    int L = 0;
+    while (L < 32 && (e >> L)) ++L;
+    int t = 0;
+    while (t < L && ((e >> (L - 1 - t)) & 1u)) ++t;
+    M.e_ones = t;
+    M.e_r = L - t;
+    M.e_low = M.e_r ? (e & ((1u << M.e_r) - 1u)) : 0u;
+    return M;
+}
+
+// per-prime constant table (Montgomery form), uploaded by the host
+constexpr int kModpTab = 96;   // [k] = k^-1 R, [32 + k] = k R (k = 1..31)
+constexpr int kModpTabK = 32;
 
 constexpr int kModpThreads = 128;
 
@@ -70,23 +116,20 @@ struct ModpLayout {  // in uint32 words
     static constexpr int TOTAL = RED + 8;  // even: every team's RED stays 8-byte aligned
 };
 
-// team sum of per-lane residues < p
+// team sum of per-lane residues < p (modular adds at every level)
 template <int W>
 __device__ __forceinline__ uint32_t team_sum_mod(const TeamCtx<W>& tc, uint32_t* red, uint32_t v,
                                                  const ModP& M) {
-    unsigned long long s = v;
     constexpr int WW = W < 32 ? W : 32;
 #pragma unroll
-    for (int off = WW / 2; off > 0; off >>= 1)
-        s += __shfl_xor_sync(0xffffffffu, s, off, WW);
+    for (int off = WW / 2; off > 0; off >>= 1) v = M.add(v, __shfl_xor_sync(0xffffffffu, v, off, WW));
     if constexpr (W > 32) {
-        if ((tc.lane & 31) == 0) reinterpret_cast<unsigned long long*>(red)[tc.lane >> 5] = s;
+        if ((tc.lane & 31) == 0) red[tc.lane >> 5] = v;
         tc.sync();
-        const unsigned long long* r = reinterpret_cast<unsigned long long*>(red);
-        s = r[0] + r[1];
+        v = M.add(red[0], red[1]);
         tc.sync();
     }
-    return M.red(s);
+    return v;
 }
 
 template <int W>
@@ -118,11 +161,12 @@ __device__ __forceinline__ uint32_t team_bcast_u32(const TeamCtx<W>& tc, uint32_
     }
 }
 
-// inv[k] = k^-1 mod p for k = 1..kDMax (from the host)
+// All residues in Montgomery form (x R mod p): atilde / diag from the host, `tab` the
+// per-prime constants (kModpTab layout).  The launch total gets plain residues.
 template <int S, bool LOOPS>
 __global__ void __launch_bounds__(kModpThreads) modp_term_kernel(
     const uint32_t* __restrict__ atilde, const uint32_t* __restrict__ diag, int n_half, ClassItems ci,
-    ModP M, const uint32_t* __restrict__ inv, unsigned long long* __restrict__ total) {
+    ModP M, const uint32_t* __restrict__ tab, unsigned long long* __restrict__ total) {
     constexpr int W = TeamWidth<S>::W;
     constexpr int TPB = kModpThreads / W;
     constexpr int MH = S / 2;
@@ -150,7 +194,7 @@ __global__ void __launch_bounds__(kModpThreads) modp_term_kernel(
     const int n = 2 * n_half;
     const int D = n_half;
     const uint32_t p = M.p;
-    const uint32_t inv2 = inv[2];
+    const uint32_t inv2 = tab[2];
     unsigned long long my_sum = 0;  // lane 0: this team's terms (each < p)
     const long long stride = (long long)gridDim.x * TPB;
 
@@ -186,10 +230,11 @@ __global__ void __launch_bounds__(kModpThreads) modp_term_kernel(
                     uint32_t* ub = U + (k & 1) * S;
                     if (lane < S) ub[lane] = u;
                     tc.sync();
-                    unsigned long long acc = 0;
+                    uint32_t acc = 0u;
                     if (lane < S)
-                        for (int i = 0; i < S; ++i) acc += M.mul(ub[i], H[lane * LD + i]);
-                    u = lane < S ? M.red(acc) : 0u;
+                        for (int i = 0; i < S; i += 2)  // S even: products in pairs, one REDC each
+                            acc = M.add(acc, M.mul2(ub[i], H[lane * LD + i], ub[i + 1], H[lane * LD + i + 1]));
+                    u = acc;
                 }
             }
         }
@@ -227,22 +272,32 @@ __global__ void __launch_bounds__(kModpThreads) modp_term_kernel(
             }
             const uint32_t piv = team_bcast_u32<W>(tc, RED, x, plane);
             const uint32_t pv1 = team_bcast_u32<W>(tc, RED, x1, plane);
-            const uint32_t ipiv = M.pow(piv, p - 2);
+            const uint32_t ipiv = M.inv(piv);
             const bool elim = myrow >= J + 2 && myrow < S;
             const uint32_t mu = elim ? M.mul(x, ipiv) : 0u;
             if (elim) MUS[myrow] = mu;
             tc.sync();
             const uint32_t* prw = H + plane;
             uint32_t acc = 0;
-            unsigned long long acc64 = 0;
+            int c = J + 2;
 #pragma unroll 1
-            for (int c = J + 2; c < S; ++c) {
+            for (; c + 1 < S; c += 2) {  // row update of two columns, their column-gemv terms in one REDC
+                const uint32_t x0 = lane < S ? H[c * LD + lane] : 0u;
+                const uint32_t x1c = lane < S ? H[(c + 1) * LD + lane] : 0u;
+                const uint32_t y0 = M.sub(x0, M.mul(mu, prw[c * LD]));
+                const uint32_t y1 = M.sub(x1c, M.mul(mu, prw[(c + 1) * LD]));
+                acc = M.add(acc, M.mul2(MUS[c], y0, MUS[c + 1], y1));
+                if (elim) {
+                    H[c * LD + lane] = y0;
+                    H[(c + 1) * LD + lane] = y1;
+                }
+            }
+            if (c < S) {
                 const uint32_t xc = lane < S ? H[c * LD + lane] : 0u;
                 const uint32_t y = M.sub(xc, M.mul(mu, prw[c * LD]));
-                acc64 += M.mul(MUS[c], y);
+                acc = M.add(acc, M.mul(MUS[c], y));
                 if (elim) H[c * LD + lane] = y;
             }
-            acc = M.red(acc64);
             const uint32_t h1 = M.add(M.sub(x1, M.mul(mu, pv1)), acc);
             if constexpr (W > 32) tc.sync();
             if (lane < S) H[(J + 1) * LD + lane] = h1;
@@ -251,14 +306,14 @@ __global__ void __launch_bounds__(kModpThreads) modp_term_kernel(
         const uint32_t* lmf = ws + L::LM + ((S - 2) & 1) * S;
         auto h = [&](int i, int c) -> uint32_t { return H[c * LD + lmf[i]]; };
         // ------------------------------------------------ characteristic polynomial (leading minors)
-        if (lane == 0) PT[0] = 1u;
-        uint32_t prodl = 1u;
+        if (lane == 0) PT[0] = M.one;
+        uint32_t prodl = M.one;
         tc.sync();
         for (int k = 1; k <= S; ++k) {
             if (k >= 2) {
                 const uint32_t beta = h(k - 1, k - 2);
                 if (lane <= k - 2) {
-                    prodl = M.mul(lane == k - 2 ? 1u : prodl, beta);
+                    prodl = M.mul(lane == k - 2 ? M.one : prodl, beta);
                     CF[lane] = M.mul(h(lane, k - 1), prodl);  // coef of P_{lane}
                 }
             }
@@ -272,9 +327,12 @@ __global__ void __launch_bounds__(kModpThreads) modp_term_kernel(
                     v = Pk1[k - 1];
                 } else {
                     v = M.sub(d >= 1 ? Pk1[d - 1] : 0u, M.mul(hk, Pk1[d]));
-                    unsigned long long s = 0;
-                    for (int i = d + 1; i < k; ++i) s += M.mul(CF[i - 1], PT[((i - 1) * i) / 2 + d]);
-                    v = M.sub(v, M.red(s));
+                    uint32_t s = 0u;
+                    int i = d + 1;
+                    for (; i + 1 < k; i += 2)
+                        s = M.add(s, M.mul2(CF[i - 1], PT[((i - 1) * i) / 2 + d], CF[i], PT[(i * (i + 1)) / 2 + d]));
+                    if (i < k) s = M.add(s, M.mul(CF[i - 1], PT[((i - 1) * i) / 2 + d]));
+                    v = M.sub(v, s);
                 }
                 Pk[d] = v;
             }
@@ -287,7 +345,7 @@ __global__ void __launch_bounds__(kModpThreads) modp_term_kernel(
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const int k = lane + 1 + W * r;
-                acck[r] = (k <= D && k <= S) ? M.sub(0u, M.mul((uint32_t)k, a[S - k])) : 0u;
+                acck[r] = (k <= D && k <= S) ? M.sub(0u, M.mul(tab[kModpTabK + k], a[S - k])) : 0u;
             }
             for (int kk = 1; kk <= D; ++kk) {
                 const int owner = (kk - 1) % W, chunk = (kk - 1) / W;
@@ -308,9 +366,9 @@ __global__ void __launch_bounds__(kModpThreads) modp_term_kernel(
         tc.sync();
         // g_k = k s_k = t_k / 2 (+ k ell_k / 2)
         for (int k = lane + 1; k <= D; k += W) {
-            uint32_t g = M.mul(T[k], inv2);
-            if constexpr (LOOPS) g = M.add(g, M.mul(M.mul((uint32_t)k, G[k]), inv2));
-            G[k] = g;
+            uint32_t t = T[k];
+            if constexpr (LOOPS) t = M.add(t, M.mul(tab[kModpTabK + k], G[k]));
+            G[k] = M.mul(t, inv2);
         }
         tc.sync();
         // ------------------------------------------------ exp: e_k = k^-1 sum_{j=1..k} g_j e_{k-j}
@@ -322,14 +380,14 @@ __global__ void __launch_bounds__(kModpThreads) modp_term_kernel(
             for (int kk = 0; kk < D; ++kk) {
                 uint32_t ek;
                 if (kk == 0) {
-                    ek = 1u;
+                    ek = M.one;
                 } else {
                     const int owner = (kk - 1) % W, chunk = (kk - 1) / W;
                     uint32_t v = acck[0];
 #pragma unroll
                     for (int r = 1; r < R; ++r)
                         if (r == chunk) v = acck[r];
-                    ek = M.mul(team_bcast_u32<W>(tc, RED, v, owner), inv[kk]);
+                    ek = M.mul(team_bcast_u32<W>(tc, RED, v, owner), tab[kk]);
                 }
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
@@ -342,7 +400,7 @@ __global__ void __launch_bounds__(kModpThreads) modp_term_kernel(
 #pragma unroll
             for (int r = 1; r < R; ++r)
                 if (r == chunk) v = acck[r];
-            eD = M.mul(team_bcast_u32<W>(tc, RED, v, owner), inv[D]);
+            eD = M.redc(M.mul(team_bcast_u32<W>(tc, RED, v, owner), tab[D]));  // plain residue
         }
         if (valid && lane == 0) my_sum += ((D - MH) & 1) ? (eD ? p - eD : 0u) : eD;
         tc.sync();

@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=SEED_DEFAULT)
     ap.add_argument("--arith", choices=["fast", "mirror"], default="fast")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--exact-steps", type=int, default=3,
+                    help="timed runs of the exact GF(p) mode on cfg3 (0 = skip)")
     ap.add_argument("--mirror-steps", type=int, default=1,
                     help="timed steps in bit-exact MIRROR arithmetic (0 = skip)")
     return ap.parse_args()
@@ -344,6 +346,24 @@ def run_ours(args):
                           "terms and partials are bit-identical to hafnium's numba kernels "
                           "(tests/test_gpu_parity.py)"}
 
+    # exact GF(p)+CRT mode on cfg3 (integer matching count, beyond float precision)
+    exact_line = None
+    if rank == 0 and args.exact_steps > 0:
+        from paper_1805_12498_b200 import exact as X, workloads
+
+        a3 = workloads.cfg3()
+        X.hafnian_exact(a3)  # warm-up
+        ts = []
+        for _ in range(args.exact_steps):
+            t0 = time.perf_counter()
+            cnt3 = X.hafnian_exact(a3)
+            ts.append(time.perf_counter() - t0)
+        t3 = statistics.median(ts)
+        exact_line = {"workload": "cfg3: perfect matchings of an ER(0.5) n=40 graph (seed 2)",
+                      "value": (2**20 - 1) / t3, "unit": "subset-terms/s (3 primes, host prep included)",
+                      "sec": t3, "result": str(cnt3),
+                      "matches_known_answer": cnt3 == 308544357990268074}
+
     cpu = None
     if rank == 0 and world == 1:
         from oracle import oracle as O
@@ -385,6 +405,8 @@ def run_ours(args):
         }
         if mirror is not None:
             line["mirror"] = mirror
+        if exact_line is not None:
+            line["exact"] = exact_line
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)

@@ -422,7 +422,7 @@ int enqueue_mask_range(const cd* at, const cd* dg, int n_half, uint64_t lo, uint
     }
     uint64_t width = (hi - lo + n_chunks - 1) / n_chunks;
     int thr = 128;
-    range_kahan_kernel<<<(n_chunks + thr - 1) / thr, thr, 0, st>>>(terms, status, lo, hi, width,
+    range_kahan_kernel<<<(n_chunks + 3) / 4, thr, 0, st>>>(terms, status, lo, hi, width,
                                                                      n_chunks, 1, count, partials,
                                                                      fails);
     ++g_launches;
@@ -470,7 +470,7 @@ int enqueue_range_list(const cd* at, const cd* dg, int n_half, int n_ranges, con
     }
     if (terms_done) CK(cudaEventRecord(terms_done, st));
     int thr = 128;
-    list_kahan_kernel<<<(count + thr - 1) / thr, thr, 0, st>>>(terms, status, d_ranges, count, width,
+    list_kahan_kernel<<<(count + 3) / 4, thr, 0, st>>>(terms, status, d_ranges, count, width,
                                                                total, partials, fails);
     ++g_launches;
     CK(cudaGetLastError());
@@ -703,7 +703,7 @@ int hafb_sum_subsets_fast(const double* atilde, const double* diag, int n_half, 
         CK(launch_terms(backend, include_loops, d_at, d_dg, n_half, plain_map(1), count, count,
                         cap_mult, 0, 0, terms, status, c.st));
     }
-    worker_kahan_kernel<<<(workers + 127) / 128, 128, 0, c.st>>>(terms, status, total, width,
+    worker_kahan_kernel<<<(workers + 3) / 4, 128, 0, c.st>>>(terms, status, total, width,
                                                                  n_ranges, workers, d_sum, d_fail);
     ++g_launches;
     CK(cudaGetLastError());
@@ -833,7 +833,7 @@ int hafb_batch(const double* atilde, const double* diag, int batch, int n_half, 
     // problem b's term for mask q+1 sits at b*per + q: the reduce runs with lo = 1
     {
         int thr = 128;
-        int blocks = (int)(((long long)n_ranges * batch + thr - 1) / thr);
+        int blocks = (int)(((long long)n_ranges * batch + 3) / 4);  // one warp per range
         range_kahan_kernel<<<blocks, thr, 0, c.st>>>(d_t, d_s, 1, total, width, n_ranges, batch,
                                                      per, d_part, d_fail);
         ++g_launches;

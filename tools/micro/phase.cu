@@ -18,7 +18,7 @@ int main(int argc, char** argv) {
     srand(1);
     for (int i = 0; i < n; ++i) for (int j = 0; j <= i; ++j) { cd v = mk((rand() / (double)RAND_MAX - 0.5) / 7, (rand() / (double)RAND_MAX - 0.5) / 7); at[i * n + j] = v; at[j * n + i] = v; }
     for (int i = 0; i < n; ++i) { at[i * n + i] = mk(0, 0); dg[i] = mk(0, 0); }
-    unsigned long long lo = 0, hi = 1ull << 20;
+    unsigned long long lo = 0, hi = 1ull << (argc > 1 ? atoi(argv[1]) : 20);
     Seg sg{lo, hi, 0};
     long long prefix[2] = {0, (long long)(cb(hi, m, D) - cb(lo, m, D))};
     unsigned long long base[1] = {cb(lo, m, D)};

@@ -405,6 +405,7 @@ int enqueue_mask_range(const cd* at, const cd* dg, int n_half, uint64_t lo, uint
     cd* terms;
     int8_t* status;
     carve_terms_ws(ws, count, &terms, &status);
+    CK(cudaMemsetAsync(status, 0, (size_t)std::max<long long>(count, 1), st));  // kernels write failures only
     if (count > 0) {
         if (use_class_path(backend)) {
             std::vector<Seg> segs(1);
@@ -442,6 +443,7 @@ int enqueue_range_list(const cd* at, const cd* dg, int n_half, int n_ranges, con
     cd* terms;
     int8_t* status;
     carve_terms_ws(ws, items, &terms, &status);
+    CK(cudaMemsetAsync(status, 0, (size_t)std::max<long long>(items, 1), st));  // kernels write failures only
     char* tw = static_cast<char*>(ws) + terms_ws_bytes(items);
     int32_t* d_ranges = reinterpret_cast<int32_t*>(tw + table_ws_bytes(n_half, count));
     CK(cudaMemcpyAsync(d_ranges, h_ranges, sizeof(int32_t) * count, cudaMemcpyHostToDevice, st));
@@ -690,6 +692,7 @@ int hafb_sum_subsets_fast(const double* atilde, const double* diag, int n_half, 
     CK(cudaMemcpyAsync(d_at, atilde, sizeof(cd) * n * n, cudaMemcpyHostToDevice, c.st));
     CK(cudaMemcpyAsync(d_dg, diag, sizeof(cd) * n, cudaMemcpyHostToDevice, c.st));
     carve_terms_ws(d_ws, count, &terms, &status);
+    CK(cudaMemsetAsync(status, 0, (size_t)std::max<long long>(count, 1), c.st));  // kernels write failures only
     if (use_class_path(backend)) {
         std::vector<Seg> segs(1);
         segs[0].lo = 1;
@@ -737,6 +740,7 @@ int hafb_terms(const double* atilde, const double* diag, int n_half, const uint6
     CK(c.alloc(&d_m, sizeof(uint32_t) * count));
     CK(c.alloc(&d_t, sizeof(cd) * count));
     CK(c.alloc(&d_s, count));
+    CK(cudaMemsetAsync(d_s, 0, (size_t)count, c.st));  // kernels write failures only
     CK(cudaMemcpyAsync(d_at, atilde, sizeof(cd) * n * n, cudaMemcpyHostToDevice, c.st));
     CK(cudaMemcpyAsync(d_dg, diag, sizeof(cd) * n, cudaMemcpyHostToDevice, c.st));
     CK(cudaMemcpyAsync(d_m, h_masks.data(), sizeof(uint32_t) * count, cudaMemcpyHostToDevice, c.st));
@@ -813,6 +817,7 @@ int hafb_batch(const double* atilde, const double* diag, int batch, int n_half, 
     CK(c.alloc(&d_dg, sizeof(cd) * n * (size_t)batch));
     CK(c.alloc(&d_t, sizeof(cd) * cnt));
     CK(c.alloc(&d_s, cnt));
+    CK(cudaMemsetAsync(d_s, 0, cnt, c.st));  // kernels write failures only
     CK(c.alloc(&d_part, sizeof(cd) * n_ranges * (size_t)batch));
     CK(c.alloc(&d_fail, sizeof(long long) * n_ranges * (size_t)batch));
     CK(c.alloc(&d_res, sizeof(cd) * batch));

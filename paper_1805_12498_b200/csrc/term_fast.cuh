@@ -783,7 +783,7 @@ __global__ void __launch_bounds__(kFastThreads) fast_term_kernel(const cd* __res
         if (valid && lane == ((D - 1) % W)) {
             const bool neg = ((D - M) & 1) != 0;
             terms[ir.out] = bad ? mk(0.0, 0.0) : (neg ? mk(-eD.re, -eD.im) : eD);
-            status[ir.out] = bad ? 2 : 0;
+            if (bad) status[ir.out] = 2;  // the buffer is zeroed by the host (no scattered byte writes)
         }
         tc.sync();
         HT_MARK(4);

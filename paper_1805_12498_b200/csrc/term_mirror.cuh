@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(kMirrorThreads) mirror_term_kernel(
             const cd coeff = E[D];
             const bool neg = ((D - M) & 1) != 0;
             terms[ir.out] = bad ? mk(0.0, 0.0) : (neg ? m_neg(coeff) : coeff);
-            status[ir.out] = bad ? 2 : 0;
+            if (bad) status[ir.out] = 2;  // the buffer is zeroed by the host
         }
         tc.sync();
     }

@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(256) terms_smem_kernel(
                                              mask, cap_mult, w, lane, t, st);
         if (lane == 0) {
             terms[it] = t;
-            status[it] = (int8_t)st;
+            if (st) status[it] = (int8_t)st;  // the buffer is zeroed by the host
         }
         __syncwarp();
     }
@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(256) terms_smem_class_kernel(
                                          cap_mult, w, lane, t, st);
         if (lane == 0) {
             terms[ir.out] = t;
-            status[ir.out] = (int8_t)st;
+            if (st) status[ir.out] = (int8_t)st;  // the buffer is zeroed by the host
         }
         __syncwarp();
     }

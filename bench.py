@@ -42,6 +42,10 @@ sys.path.insert(0, REPO)
 
 N_DEFAULT, SEED_DEFAULT, N_RANGES = 52, 3, 512
 METRIC = "subset-terms/sec (n=52 hafnian)"
+
+
+def metric_name(n: int) -> str:
+    return METRIC if n == N_DEFAULT else f"subset-terms/sec (n={n} hafnian)"
 UNIT = "terms/s"
 
 
@@ -121,7 +125,7 @@ def run_reference(args):
             desc = f"{count} uniform random masks of the n={args.n} problem per step ({dt:.1f} s)"
     value = statistics.median(rates)
     print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "impl": "reference", "metric": metric_name(args.n), "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * ((1 << nh) - 1) / value, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64 (complex128)",
@@ -380,13 +384,15 @@ def run_ours(args):
     tpath = os.path.join(REPO, "profiles", "roofline_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get("bytes_per_step")
+            # measured DRAM bytes per term of the term kernels (profiles/roofline_traffic.json),
+            # per launch-set of one step
+            traffic = json.load(open(tpath)).get("bytes_per_term") * nterms
         except (ValueError, OSError):
             traffic = None
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "metric": metric_name(args.n), "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_max / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64 (complex128)", "data": "synthetic (seeded, SURVEY.md Appendix A)",

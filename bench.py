@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=SEED_DEFAULT)
     ap.add_argument("--arith", choices=["fast", "mirror"], default="fast")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--parity-bits", type=int, default=20,
+                    help="check FAST/MIRROR against the CPU oracle on masks [0, 2^bits) (0 = skip)")
     ap.add_argument("--exact-steps", type=int, default=3,
                     help="timed runs of the exact GF(p) mode on cfg3 (0 = skip)")
     ap.add_argument("--mirror-steps", type=int, default=1,
@@ -368,6 +370,45 @@ def run_ours(args):
                       "sec": t3, "result": str(cnt3),
                       "matches_known_answer": cnt3 == 308544357990268074}
 
+    # parity at full size (north star: identical contiguous subset range at n >= 48):
+    # FAST and MIRROR against the CPU oracle (bit-pinned to the reference) on [0, 2^20)
+    parity = None
+    if rank == 0 and args.parity_bits > 0:
+        from oracle import oracle as O
+
+        O.build()
+        hi = 1 << min(args.parity_bits, nh)
+        masks = np.arange(1, hi, dtype=np.uint64)
+        thr = len(os.sched_getaffinity(0))
+        t_orc = O.terms(at, dg, nh, masks, backend=1, threads=thr)[0]
+        t_fast, _ = kernels.terms(at, dg, nh, masks, 1, False, arith="fast", device=local)
+        t_mir, _ = kernels.terms(at, dg, nh, masks, 1, False, arith="mirror", device=local)
+        n_ch = 8
+        r_orc = O.tree_reduce(O.sum_mask_range(at, dg, nh, 0, hi, n_ch, 1, False)[0])
+        r_fast = engine.tree_reduce(kernels.sum_mask_range(at, dg, nh, 0, hi, n_ch, 1, False,
+                                                               arith="fast", device=local)[0])
+        r_mir = engine.tree_reduce(kernels.sum_mask_range(at, dg, nh, 0, hi, n_ch, 1, False,
+                                                              arith="mirror", device=local)[0])
+        abs_sum = float(np.abs(t_orc).sum())
+        den = np.maximum(np.abs(t_orc), 1e-300)
+        parity = {
+            "range": f"masks [0, 2^{min(args.parity_bits, nh)}) of the n={args.n} workload, "
+                     f"{n_ch} Kahan chunks + fixed tree (SURVEY.md 8(c) harness)",
+            "oracle": "oracle/hafnian_oracle.c (bit-identical to hafnium.kernels._numba on the "
+                      "golden fixtures), charpoly backend",
+            "tolerance": 1e-10,
+            "fast_rel_err": abs(r_fast - r_orc) / abs(r_orc),
+            "fast_abs_sum_normalised_err": abs(r_fast - r_orc) / abs_sum,
+            "fast_max_term_rel_err": float((np.abs(t_fast - t_orc) / den).max()),
+            "mirror_bit_identical_result": bool(r_mir == r_orc),
+            "mirror_bit_identical_terms": int((np.ascontiguousarray(t_mir).view(np.uint64).reshape(-1, 2)
+                                               == np.ascontiguousarray(t_orc).view(np.uint64).reshape(-1, 2))
+                                              .all(axis=1).sum()),
+            "terms": int(masks.size),
+            "cond_abs_sum_over_result": abs_sum / abs(r_orc),
+        }
+        parity["pass"] = parity["fast_rel_err"] <= 1e-10 and parity["mirror_bit_identical_result"]
+
     cpu = None
     if rank == 0 and world == 1:
         from oracle import oracle as O
@@ -413,6 +454,8 @@ def run_ours(args):
             line["mirror"] = mirror
         if exact_line is not None:
             line["exact"] = exact_line
+        if parity is not None:
+            line["parity"] = parity
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)

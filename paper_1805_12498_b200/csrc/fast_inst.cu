@@ -10,28 +10,40 @@
 
 namespace hafb {
 
-// Hessenberg variant per size (measured on B200, tools/micro/phase.cu): the
-// shared-memory reduction wins for 18 <= S <= 26 and S >= 34, the register-window
-// reduction elsewhere.
-constexpr bool smem_hess(int S) { return (S >= 18 && S <= 26) || S >= 34; }
+// Hessenberg variant per size (measured on B200, tools/class_time.py under ncu): the
+// shared-memory reduction wins for 18 <= S <= 24 and S >= 34 (these classes are
+// shared-memory-bandwidth bound), the register-window reduction elsewhere.
+constexpr bool smem_hess(int S) { return (S >= 18 && S <= 24) || S >= 34; }
+
+// Threads per block.  The register-window kernel for 26 <= S <= 32 runs ONE block of
+// 384 threads per SM whose teams are phase-synchronised (__syncthreads between the
+// Hessenberg, charpoly and series phases): the SM's instruction cache then holds one
+// phase's code at a time, which removed the top stall ("no instruction", 34% of
+// stall cycles at S = 30) and cut these classes by ~20%.  The shared-memory classes
+// are L1-bound and gain nothing from it (measured), so they keep 128-thread blocks.
+#ifndef HAFB_REG_THREADS
+#define HAFB_REG_THREADS 384
+#endif
+constexpr int threads_for(int S) { return !smem_hess(S) && S >= 26 ? HAFB_REG_THREADS : kFastThreads; }
 
 template <int S, bool L>
 static cudaError_t launch_one(const cd* at, const cd* dg, int n_half, const ClassItems& ci,
                               cd* terms, int8_t* status, cudaStream_t st, int sms) {
     constexpr int W = TeamWidth<S>::W;
-    constexpr int TPB = kFastThreads / W;
+    constexpr int NT = threads_for(S);
+    constexpr int TPB = NT / W;
     constexpr bool SH = smem_hess(S);
     const size_t smem = (size_t)TPB * FastLayout<S, SH, L>::TOTAL * sizeof(cd) + (kDMax + 1) * sizeof(double);
-    auto kern = fast_term_kernel<S, L, SH>;
+    auto kern = fast_term_kernel<S, L, SH, NT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int occ = 1;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kFastThreads, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);
     if (e != cudaSuccess) return e;
     const long long want = (ci.n_items + TPB - 1) / TPB;
     const long long cap_blocks = (long long)sms * std::max(occ, 1);
     const int grid = (int)std::max<long long>(1, std::min(want, cap_blocks));
-    kern<<<grid, kFastThreads, smem, st>>>(at, dg, n_half, ci, terms, status);
+    kern<<<grid, NT, smem, st>>>(at, dg, n_half, ci, terms, status);
     return cudaGetLastError();
 }
 

@@ -478,16 +478,19 @@ __device__ __forceinline__ void smem_hessenberg(cd* H, int& myrow, const TeamCtx
     tc.sync();
 }
 
-template <int S, bool LOOPS, bool SH>
-__global__ void __launch_bounds__(kFastThreads) fast_term_kernel(const cd* __restrict__ atilde,
+template <int S, bool LOOPS, bool SH, int NT = kFastThreads>
+__global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ atilde,
                                                                  const cd* __restrict__ diag,
                                                                  int n_half, ClassItems ci,
                                                                  cd* __restrict__ terms,
                                                                  int8_t* __restrict__ status) {
     constexpr int W = TeamWidth<S>::W;
-    constexpr int TPB = kFastThreads / W;
+    constexpr int TPB = NT / W;
     constexpr int M = S / 2;
     constexpr int R = (kDMax + W - 1) / W;  // coefficient chunks per lane
+    // blocks of more than 128 threads (one block per SM) keep their teams in the same
+    // phase so the SM's instruction cache holds one phase's code at a time
+    constexpr bool PSYNC = NT > kFastThreads;
     using L = FastLayout<S, SH, LOOPS>;
     extern __shared__ cd smem[];
     TeamCtx<W> tc;
@@ -600,6 +603,7 @@ __global__ void __launch_bounds__(kFastThreads) fast_term_kernel(const cd* __res
             fast_hessenberg<S, W>(hr, myrow, tc, ws);
         }
         HT_MARK(1);
+        if constexpr (PSYNC) __syncthreads();
         tc.sync();
         // ---------------------------------------------- charpoly (_numba.py:203-225)
         {
@@ -669,6 +673,7 @@ __global__ void __launch_bounds__(kFastThreads) fast_term_kernel(const cd* __res
             tc.sync();
         }
         HT_MARK(2);
+        if constexpr (PSYNC) __syncthreads();
         // ---------------------------------------------- Newton + Cayley-Hamilton (_numba.py:228-250)
         cd* T = ws + L::T;
         cd* A = ws + L::A;

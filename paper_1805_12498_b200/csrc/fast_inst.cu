@@ -13,7 +13,10 @@ namespace hafb {
 // Hessenberg variant per size (measured on B200, tools/class_time.py under ncu): the
 // shared-memory reduction wins for 18 <= S <= 24 and S >= 34 (these classes are
 // shared-memory-bandwidth bound), the register-window reduction elsewhere.
-constexpr bool smem_hess(int S) { return (S >= 18 && S <= 24) || S >= 34; }
+#ifndef HAFB_SMEM_HI
+#define HAFB_SMEM_HI 34
+#endif
+constexpr bool smem_hess(int S) { return (S >= 18 && S <= 24) || S >= HAFB_SMEM_HI; }
 
 // Threads per block.  The register-window kernel for 26 <= S <= 32 runs ONE block of
 // 384 threads per SM whose teams are phase-synchronised (__syncthreads between the
@@ -24,7 +27,7 @@ constexpr bool smem_hess(int S) { return (S >= 18 && S <= 24) || S >= 34; }
 #ifndef HAFB_REG_THREADS
 #define HAFB_REG_THREADS 384
 #endif
-constexpr int threads_for(int S) { return !smem_hess(S) && S >= 26 ? HAFB_REG_THREADS : kFastThreads; }
+constexpr int threads_for(int S) { return !smem_hess(S) && S >= 26 ? (S > 32 ? 256 : HAFB_REG_THREADS) : kFastThreads; }
 
 template <int S, bool L>
 static cudaError_t launch_one(const cd* at, const cd* dg, int n_half, const ClassItems& ci,

@@ -14,7 +14,7 @@ template <int S, bool L>
 static cudaError_t launch_one(const cd* at, const cd* dg, int n_half, const ClassItems& ci,
                               cd* terms, int8_t* status, cudaStream_t st, int sms) {
     constexpr int W = TeamWidth<S>::W;
-    constexpr int TPB = kMirrorThreads / W > 0 ? kMirrorThreads / W : 1;
+    constexpr int TPB = mirror_tpb<S>();
     constexpr int THREADS = TPB * W;
     const size_t smem = (size_t)TPB * MirrorLayout<S>::TOTAL * sizeof(cd);
     auto kern = mirror_term_kernel<S, L>;

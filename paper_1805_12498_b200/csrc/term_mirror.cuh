@@ -31,14 +31,26 @@ namespace hafb {
 
 constexpr int kMirrorThreads = 64;
 
+// teams per block: one team per block from W = 32 up (the kernel is latency-bound and
+// shared-memory-limited, so single-team blocks let leftover shared memory host one
+// more team per SM); small teams share 64-thread blocks
+template <int S>
+constexpr int mirror_tpb() {
+    return TeamWidth<S>::W >= 32 ? 1 : kMirrorThreads / TeamWidth<S>::W;
+}
+
 template <int S>
 struct MirrorLayout {
     static constexpr int LD = S + 1;                     // odd column stride: conflict-free
     static constexpr int TRI = (S + 1) * (S + 2) / 2;    // triangular tables
+    // region A: the S x S subset matrix during the Hessenberg reduction, then (after
+    // the reduced form is packed into HS) the charpoly tables CF and P
+    static constexpr int AREA = S * LD > (S + 1) * (S + 1) ? S * LD : (S + 1) * (S + 1);
     static constexpr int H = 0;                          // S columns x LD
-    static constexpr int CF = H + S * LD;                // coef_{k,i}: row k at k(k-1)/2
-    static constexpr int P = CF + TRI;                   // P_k: row k at k(k+1)/2, length k+1
-    static constexpr int MU = P + TRI;                   // [S+2] multipliers by logical row
+    static constexpr int CF = 0;                         // coef_{k,i}: row k at k(k-1)/2 (S(S+1)/2)
+    static constexpr int P = S * (S + 1) / 2;            // P_k: row k at k(k+1)/2, length k+1
+    static constexpr int HS = AREA;                      // packed upper Hessenberg: column c at c(c+3)/2
+    static constexpr int MU = HS + (S - 1) * (S + 2) / 2 + S;  // [S+2] multipliers by logical row
     static constexpr int T = MU + S + 2;                 // [kDMax+2] traces
     static constexpr int SS = T + kDMax + 2;             // [kDMax+2] series
     static constexpr int E = SS + kDMax + 2;             // [kDMax+2] exp Horner state
@@ -105,7 +117,7 @@ __global__ void __launch_bounds__(kMirrorThreads) mirror_term_kernel(
     const cd* __restrict__ atilde, const cd* __restrict__ diag, int n_half, ClassItems ci,
     cd* __restrict__ terms, int8_t* __restrict__ status) {
     constexpr int W = TeamWidth<S>::W;
-    constexpr int TPB = kMirrorThreads / W > 0 ? kMirrorThreads / W : 1;
+    constexpr int TPB = mirror_tpb<S>();
     constexpr int M = S / 2;
     using L = MirrorLayout<S>;
     constexpr int LD = L::LD;
@@ -258,7 +270,14 @@ __global__ void __launch_bounds__(kMirrorThreads) mirror_term_kernel(
             tc.sync();
         }
         const int* lmf = LM0 + ((S - 2) & 1) * S;  // final logical row -> lane
-        auto h = [&](int i, int c) -> cd { return H[c * LD + lmf[i]]; };
+        // pack the reduced (upper Hessenberg) form: logical row i, columns c >= i-1
+        cd* HSp = ws + L::HS;
+        if (lane < S) {
+            const int ph = lmf[lane];
+            for (int c = lane > 0 ? lane - 1 : 0; c < S; ++c) HSp[(c * (c + 3)) / 2 + lane] = H[c * LD + ph];
+        }
+        tc.sync();  // region A is reused by CF / P from here on
+        auto h = [&](int i, int c) -> cd { return HSp[(c * (c + 3)) / 2 + i]; };
         // ------------------------------------------------ charpoly (_numba.py:203-225)
         // (1) coefficient chains: lane k-1 walks prod/coef of P_k, i = k-1 .. 1
         if (lane < S) {

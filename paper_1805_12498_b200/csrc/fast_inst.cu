@@ -27,7 +27,12 @@ constexpr bool smem_hess(int S) { return (S >= 18 && S <= 24) || S >= HAFB_SMEM_
 #ifndef HAFB_REG_THREADS
 #define HAFB_REG_THREADS 384
 #endif
-constexpr int threads_for(int S) { return !smem_hess(S) && S >= 26 ? (S > 32 ? 256 : HAFB_REG_THREADS) : kFastThreads; }
+constexpr int threads_for(int S) {
+    return !smem_hess(S) && S >= 26 ? (S > 32 ? 256 : HAFB_REG_THREADS)
+           : S > 32 ? 64  // 64-lane teams: one team per block (register-limited: 5 teams/SM, not 4)
+           : smem_hess(S) ? 32  // one team per block: the register file packs one more team
+           : kFastThreads;
+}
 
 template <int S, bool L>
 static cudaError_t launch_one(const cd* at, const cd* dg, int n_half, const ClassItems& ci,

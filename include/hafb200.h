@@ -126,6 +126,17 @@ int hafb_sum_range_list_async(const double* d_atilde, const double* d_diag, int 
                               size_t workspace_bytes, double* d_partials, int64_t* d_fails,
                               void* stream, void* terms_done_event);
 
+/* hafb_batch on RAW matrices: the input semantics of matrix.py:93-115 (strict
+ * symmetry check max|A - A^T| <= symmetry_rtol * max(1, max|A|), upper -> lower
+ * mirror) and engine.py:140-150 (zeroed diagonal for the hafnian, loop weights,
+ * pair swap) run on the device.  a: batch x n x n complex128 (interleaved).  If a
+ * matrix fails the check, *asym_index is its index (first one), *asym_dev / *asym_tol
+ * the values, and nothing is computed; otherwise *asym_index = -1. */
+int hafb_batch_raw(const double* a, int batch, int n_half, int backend, int include_loops,
+                   int n_ranges, int cap_mult, int arith, int device, double symmetry_rtol,
+                   double* results, int64_t* fails, int64_t* asym_index, double* asym_dev,
+                   double* asym_tol);
+
 /* Exact mode for INTEGER matrices (no reference counterpart:
  * the reference returns a float, inexact beyond 2^53, e.g. cfg3).  The subset sum
  * of engine.py:153-178 evaluated in GF(p) for each prime: per subset the same

@@ -54,6 +54,8 @@ SIGNATURES = {
                                          _int, _vp, _size, _vp, _vp, _vp, _vp]),
     "hafb_launch_count": (_i64, [_int]),
     "hafb_fp64_peak": (_int, [_int, _dp, _dp]),
+    "hafb_batch_raw": (_int, [_dp, _int, _int, _int, _int, _int, _int, _int, _int, ctypes.c_double,
+                              _dp, _i64p, _i64p, _dp, _dp]),
     "hafb_modp_sums": (_int, [_u32p, _u32p, _u32p, _int, _int, _u64, _u64, _int, _int, _u64p, _dp]),
 }
 

@@ -792,44 +792,88 @@ int hafb_terms(const double* atilde, const double* diag, int n_half, const uint6
     return HAFB_OK;
 }
 
-int hafb_batch(const double* atilde, const double* diag, int batch, int n_half, int backend,
-               int include_loops, int n_ranges, int cap_mult, int arith, int device,
-               double* results, int64_t* fails) {
-    g_err.clear();
-    int rc = check_common(n_half, backend, arith);
-    if (rc) return rc;
-    if (batch <= 0) return HAFB_OK;
-    if (n_ranges < 1) return fail(HAFB_ERR_ARG, "n_ranges must be >= 1");
+}  // extern "C"
+
+namespace {
+
+// matrix.py:93-115 (strict mode) + engine.py:140-150 for one matrix per block: the
+// symmetry deviation max|A - A^T| and max|A| (numpy's abs = glibc hypot, NaN
+// propagating like numpy's max), the upper -> lower mirror, the zeroed diagonal
+// (hafnian), the loop weights, and the pair swap X.A.
+__device__ __forceinline__ double nan_max(double a, double b) {
+    return (a != a || b != b) ? __longlong_as_double(0x7ff8000000000000ll) : (a > b ? a : b);
+}
+
+__global__ void __launch_bounds__(128) batch_prep_kernel(const cd* __restrict__ raw, int n, int loops,
+                                                         cd* __restrict__ at, cd* __restrict__ dg,
+                                                         double* __restrict__ devmax) {
+    __shared__ double red[2][4];
+    const int b = blockIdx.x;
+    const cd* a = raw + (size_t)b * n * n;
+    cd* t = at + (size_t)b * n * n;
+    double dev = 0.0, amax = 0.0;
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+        const int i = e / n, j = e - i * n;
+        const cd v = a[e], w = a[j * n + i];
+        amax = nan_max(amax, m_abs(v));
+        dev = nan_max(dev, m_abs(m_sub(v, w)));
+        cd m = i > j ? w : v;  // the lower triangle takes the upper one
+        if (i == j) {
+            if (!loops) m = mk(0.0, 0.0);
+            dg[(size_t)b * n + i] = m;
+        }
+        t[(i ^ 1) * n + j] = m;  // X.A: row r of Atilde is row r^1 of A
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        dev = nan_max(dev, __shfl_xor_sync(0xffffffffu, dev, off));
+        amax = nan_max(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = dev;
+        red[1][threadIdx.x >> 5] = amax;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double d = red[0][0], m = red[1][0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+            d = nan_max(d, red[0][w]);
+            m = nan_max(m, red[1][w]);
+        }
+        devmax[2 * b] = d;
+        devmax[2 * b + 1] = m;
+    }
+}
+
+// the batched pipeline on prepared device inputs: terms, Kahan per range, fixed tree
+int batch_run(Call& c, const cd* d_at, const cd* d_dg, int batch, int n_half, int backend,
+              int include_loops, int n_ranges, int cap_mult, int arith, double* results,
+              int64_t* fails) {
     const int n = 2 * n_half;
     const uint64_t total = 1ull << n_half;
     const long long per = (long long)(total - 1);
     const size_t cnt = (size_t)batch * per;
     const uint64_t width = std_width(n_half, n_ranges);
     std::vector<long long> h_fail((size_t)batch * n_ranges);
-    Call c;
-    cd *d_at, *d_dg, *d_t, *d_part, *d_res;
+    cd *d_t, *d_part, *d_res;
     int8_t* d_s;
     long long* d_fail;
     void* d_tab;
-    CK(c.open(device));
     CK(c.alloc(&d_tab, table_ws_bytes(n_half, 1)));
-    CK(c.alloc(&d_at, sizeof(cd) * n * n * (size_t)batch));
-    CK(c.alloc(&d_dg, sizeof(cd) * n * (size_t)batch));
     CK(c.alloc(&d_t, sizeof(cd) * cnt));
     CK(c.alloc(&d_s, cnt));
     CK(cudaMemsetAsync(d_s, 0, cnt, c.st));  // kernels write failures only
     CK(c.alloc(&d_part, sizeof(cd) * n_ranges * (size_t)batch));
     CK(c.alloc(&d_fail, sizeof(long long) * n_ranges * (size_t)batch));
     CK(c.alloc(&d_res, sizeof(cd) * batch));
-    CK(cudaMemcpyAsync(d_at, atilde, sizeof(cd) * n * n * (size_t)batch, cudaMemcpyHostToDevice, c.st));
-    CK(cudaMemcpyAsync(d_dg, diag, sizeof(cd) * n * (size_t)batch, cudaMemcpyHostToDevice, c.st));
+    int rc;
     if (use_class_path(backend)) {
         std::vector<Seg> segs(1);
         segs[0].lo = 1;
         segs[0].hi = total;
         segs[0].out_off = 0;
         rc = enqueue_classes(backend, arith, d_at, d_dg, n_half, segs, batch, per, (long long)n * n, n,
-                                  include_loops, cap_mult, d_t, d_s, d_tab, c.st);
+                             include_loops, cap_mult, d_t, d_s, d_tab, c.st);
         if (rc) return rc;
     } else {
         CK(launch_terms(backend, include_loops, d_at, d_dg, n_half, plain_map(1), per,
@@ -857,6 +901,70 @@ int hafb_batch(const double* atilde, const double* diag, int batch, int n_half, 
         fails[b] = mx;
     }
     return HAFB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hafb_batch(const double* atilde, const double* diag, int batch, int n_half, int backend,
+               int include_loops, int n_ranges, int cap_mult, int arith, int device,
+               double* results, int64_t* fails) {
+    g_err.clear();
+    int rc = check_common(n_half, backend, arith);
+    if (rc) return rc;
+    if (batch <= 0) return HAFB_OK;
+    if (n_ranges < 1) return fail(HAFB_ERR_ARG, "n_ranges must be >= 1");
+    const int n = 2 * n_half;
+    Call c;
+    cd *d_at, *d_dg;
+    CK(c.open(device));
+    CK(c.alloc(&d_at, sizeof(cd) * n * n * (size_t)batch));
+    CK(c.alloc(&d_dg, sizeof(cd) * n * (size_t)batch));
+    CK(cudaMemcpyAsync(d_at, atilde, sizeof(cd) * n * n * (size_t)batch, cudaMemcpyHostToDevice, c.st));
+    CK(cudaMemcpyAsync(d_dg, diag, sizeof(cd) * n * (size_t)batch, cudaMemcpyHostToDevice, c.st));
+    return batch_run(c, d_at, d_dg, batch, n_half, backend, include_loops, n_ranges, cap_mult, arith,
+                     results, fails);
+}
+
+int hafb_batch_raw(const double* a, int batch, int n_half, int backend, int include_loops,
+                   int n_ranges, int cap_mult, int arith, int device, double symmetry_rtol,
+                   double* results, int64_t* fails, int64_t* asym_index, double* asym_dev,
+                   double* asym_tol) {
+    g_err.clear();
+    int rc = check_common(n_half, backend, arith);
+    if (rc) return rc;
+    *asym_index = -1;
+    if (batch <= 0) return HAFB_OK;
+    if (n_ranges < 1) return fail(HAFB_ERR_ARG, "n_ranges must be >= 1");
+    const int n = 2 * n_half;
+    Call c;
+    cd *d_raw, *d_at, *d_dg;
+    double* d_dm;
+    std::vector<double> dm(2 * (size_t)batch);
+    CK(c.open(device));
+    CK(c.alloc(&d_raw, sizeof(cd) * n * n * (size_t)batch));
+    CK(c.alloc(&d_at, sizeof(cd) * n * n * (size_t)batch));
+    CK(c.alloc(&d_dg, sizeof(cd) * n * (size_t)batch));
+    CK(c.alloc(&d_dm, sizeof(double) * 2 * (size_t)batch));
+    CK(cudaMemcpyAsync(d_raw, a, sizeof(cd) * n * n * (size_t)batch, cudaMemcpyHostToDevice, c.st));
+    batch_prep_kernel<<<batch, 128, 0, c.st>>>(d_raw, n, include_loops, d_at, d_dg, d_dm);
+    ++g_launches;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(dm.data(), d_dm, sizeof(double) * dm.size(), cudaMemcpyDeviceToHost, c.st));
+    CK(cudaStreamSynchronize(c.st));
+    for (int b = 0; b < batch; ++b) {  // matrix.py: reject if max|A-A^T| > rtol * max(1, max|A|)
+        const double dev = dm[2 * (size_t)b], amax = dm[2 * (size_t)b + 1];
+        const double tol = symmetry_rtol * (amax != amax ? amax : std::max(1.0, amax));
+        if (dev > tol) {
+            *asym_index = b;
+            *asym_dev = dev;
+            *asym_tol = tol;
+            return HAFB_OK;
+        }
+    }
+    return batch_run(c, d_at, d_dg, batch, n_half, backend, include_loops, n_ranges, cap_mult, arith,
+                     results, fails);
 }
 
 int hafb_power_traces(const double* b, int m, int K, int backend, int cap_mult, int arith,

@@ -144,6 +144,27 @@ def batch(atilde, diag, n_half, backend, include_loops, n_ranges, cap_mult=SWEEP
     return res, fails
 
 
+def batch_raw(a, n_half, backend, include_loops, n_ranges, symmetry_rtol,
+              cap_mult=SWEEP_CAP_MULT, *, arith=None, device=None):
+    """Raw matrices (B, n, n): device-side input semantics, then hafb_batch.
+    Returns (results, fails, asym) with asym = None or (index, dev, tol)."""
+    lib = _lib.load(require_device=True)
+    A = _lib.c128(a)
+    B = A.shape[0]
+    res = np.zeros(B, np.complex128)
+    fails = np.zeros(B, np.int64)
+    idx = np.full(1, -1, np.int64)
+    dev = np.zeros(1)
+    tol = np.zeros(1)
+    _lib.check(lib.hafb_batch_raw(_lib.dptr(A), int(B), int(n_half), int(backend),
+                                  int(bool(include_loops)), int(n_ranges), int(cap_mult),
+                                  _arith_id(arith), _device(device), float(symmetry_rtol),
+                                  _lib.dptr(res), _lib.i64ptr(fails), _lib.i64ptr(idx),
+                                  _lib.dptr(dev), _lib.dptr(tol)))
+    asym = None if idx[0] < 0 else (int(idx[0]), float(dev[0]), float(tol[0]))
+    return res, fails, asym
+
+
 def power_traces_spectral(b, K, cap_mult=SWEEP_CAP_MULT, *, device=None):
     """(traces, sweeps, converged); destroys nothing (the device works on a copy).
     Replaces _numba.py:415-422.  Sweeps are reported as -1 (not tracked)."""

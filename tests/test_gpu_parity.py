@@ -94,6 +94,43 @@ def test_batch_equals_single_calls():
         assert res0[s] == complex(g[f"cfg1s{s}"]["result_b0"])
 
 
+def test_batch_device_input_semantics():
+    """hafnian_batch runs matrix.py's strict check + mirror and engine._prepare on the
+    device: same bits as the single-matrix path (which does them on the host), same
+    AsymmetricInput decision and message, loops and non-finite inputs included."""
+    from paper_1805_12498_b200.errors import AsymmetricInput
+
+    rng = np.random.default_rng(11)
+    mats = []
+    for b in range(6):
+        a = random_symmetric(12, 500 + b)
+        i, j = rng.integers(0, 12, 2)
+        if i != j:  # upper/lower differ within tolerance: the upper triangle must win
+            a[min(i, j), max(i, j)] += 1e-13
+        mats.append(a)
+    mats = np.stack(mats)
+    for loops, f in ((False, engine.hafnian), (True, engine.loop_hafnian)):
+        for arith in ("mirror", "fast"):
+            res = engine.hafnian_batch(mats, backend="charpoly", arith=arith, loops=loops)
+            for b in range(len(mats)):
+                assert res[b] == f(mats[b], backend="charpoly", arith=arith), (loops, arith, b)
+    bad = mats.copy()
+    bad[3, 0, 5] += 1e-6
+    with pytest.raises(AsymmetricInput) as e1:
+        engine.hafnian_batch(bad)
+    with pytest.raises(AsymmetricInput) as e2:
+        engine.hafnian(bad[3])
+    assert str(e1.value).startswith("matrix 3: ")
+    assert str(e1.value)[len("matrix 3: "):] == str(e2.value)
+    nanm = mats.copy()
+    nanm[1, 2, 2] = np.nan  # numpy: NaN deviation never exceeds the tolerance
+    r, fails, asym = kernels.batch_raw(nanm, 6, 1, True, 63, 1e-12)
+    assert asym is None
+    at, dg, nh = engine._prepare(nanm[1], True)
+    s1, f1 = kernels.sum_subsets_det(at, dg, nh, 1, True, 1, 63)
+    assert fails[1] == f1.max()
+
+
 def test_powertraces_mirror_bit_exact():
     g = load_golden("powertraces.npz")
     for q, case in g.items():

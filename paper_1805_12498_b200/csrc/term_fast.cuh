@@ -75,6 +75,9 @@ constexpr int kGroup = 2;
 #endif
 constexpr float kPivotThreshold = HAFB_PIVOT_TAU;  // columns per uniform branch in the Hessenberg sweep
 constexpr int kDMax = 31;
+#ifndef HAFB_SHFL_PIVOT
+#define HAFB_SHFL_PIVOT 1
+#endif
 
 // packed upper-Hessenberg storage, column-major: column c holds rows 0..min(c+1, S-1)
 // and starts at c(c+3)/2.
@@ -292,54 +295,96 @@ __device__ __forceinline__ void fast_hess_step(cd (&w)[S], const int J0, int& my
     const bool elim = myrow >= J + 2 && myrow < S;
     const cd mu = elim ? f_mul(hj, ip) : mk(0.0, 0.0);
     HT_MARK(7);
-    cd* pr = ws + L::PR + OFF * L::SP;
-    cd* mus = ws + L::MU + OFF * L::SP;
-    if (myrow == J + 1) {
-        pr[OFF + 1] = w[OFF + 1];
-        static_for<OFF + 2, S, kGroup>([&](auto gg) {
-            constexpr int c0 = decltype(gg)::value;
-            if (c0 < live) {
-                static_for<c0, (c0 + kGroup < S ? c0 + kGroup : S)>([&](auto c) {
-                    pr[c()] = w[c()];
-                    return true;
-                });
+    if constexpr (HAFB_SHFL_PIVOT && S >= 26) {
+        // the pivot row stays in the pivot lane's registers: every lane reads its entries
+        // with register shuffles inside the sweep (no serial publish through shared memory)
+        cd* mus = ws + L::MU + OFF * L::SP;
+        if (myrow == J + 1) {
+#pragma unroll
+            for (int z = 0; z < kGroup; ++z) mus[live + z] = mk(0.0, 0.0);  // pipelined over-read
+        }
+        if (elim) mus[myrow - J0] = mu;
+        tc.sync();
+        HT_MARK(10);
+        const int psrc = ((int)(threadIdx.x & 31) & ~(W - 1)) + wl;
+        auto pbc = [&](const cd& v) -> cd {
+            cd r;
+            r.re = __shfl_sync(tc.wmask, v.re, psrc);
+            r.im = __shfl_sync(tc.wmask, v.im, psrc);
+            return r;
+        };
+        const cd hj1 = f_cms(w[OFF + 1], mu, pbc(w[OFF + 1]));
+        cd acc0 = mk(0.0, 0.0), acc1 = mk(0.0, 0.0);
+        static_assert(kGroup == 2, "the pipelined sweep is written for pairs");
+        cd ma = mus[OFF + 2], mb = mus[OFF + 3];
+        static_for<OFF + 2, S, 2>([&](auto gg) {
+            constexpr int c = decltype(gg)::value;
+            if (c < live) {
+                const cd ma2 = mus[c + 2], mb2 = mus[c + 3];
+                const cd pa = pbc(w[c]);
+                w[c] = f_cms(w[c], mu, pa);
+                acc0 = f_cma(acc0, ma, w[c]);
+                if constexpr (c + 1 < S) {
+                    const cd pb = pbc(w[c + 1]);
+                    w[c + 1] = f_cms(w[c + 1], mu, pb);
+                    acc1 = f_cma(acc1, mb, w[c + 1]);
+                }
+                ma = ma2;
+                mb = mb2;
             }
             return true;
         });
+        w[OFF + 1] = f_add(hj1, f_add(acc0, acc1));
+    } else {
+        cd* pr = ws + L::PR + OFF * L::SP;
+        cd* mus = ws + L::MU + OFF * L::SP;
+        if (myrow == J + 1) {
+            pr[OFF + 1] = w[OFF + 1];
+            static_for<OFF + 2, S, kGroup>([&](auto gg) {
+                constexpr int c0 = decltype(gg)::value;
+                if (c0 < live) {
+                    static_for<c0, (c0 + kGroup < S ? c0 + kGroup : S)>([&](auto c) {
+                        pr[c()] = w[c()];
+                        return true;
+                    });
+                }
+                return true;
+            });
 #pragma unroll
-        for (int z = 0; z < kGroup; ++z) {  // zero padding past the live edge
-            pr[live + z] = mk(0.0, 0.0);
-            mus[live + z] = mk(0.0, 0.0);
-        }
-    }
-    if (elim) mus[myrow - J0] = mu;
-    tc.sync();
-    HT_MARK(10);
-    const cd hj1 = f_cms(w[OFF + 1], mu, pr[OFF + 1]);
-    cd acc0 = mk(0.0, 0.0), acc1 = mk(0.0, 0.0);
-    // pairs of columns under one uniform guard; the next pair's broadcasts are
-    // loaded before the current pair's multiply-adds (software pipelining across
-    // the guard; the padded buffers make the over-read harmless)
-    static_assert(kGroup == 2, "the pipelined sweep is written for pairs");
-    cd pa = pr[OFF + 2], ma = mus[OFF + 2], pb = pr[OFF + 3], mb = mus[OFF + 3];
-    static_for<OFF + 2, S, 2>([&](auto gg) {
-        constexpr int c = decltype(gg)::value;
-        if (c < live) {
-            const cd pa2 = pr[c + 2], ma2 = mus[c + 2], pb2 = pr[c + 3], mb2 = mus[c + 3];
-            w[c] = f_cms(w[c], mu, pa);
-            acc0 = f_cma(acc0, ma, w[c]);
-            if constexpr (c + 1 < S) {
-                w[c + 1] = f_cms(w[c + 1], mu, pb);
-                acc1 = f_cma(acc1, mb, w[c + 1]);
+            for (int z = 0; z < kGroup; ++z) {  // zero padding past the live edge
+                pr[live + z] = mk(0.0, 0.0);
+                mus[live + z] = mk(0.0, 0.0);
             }
-            pa = pa2;
-            ma = ma2;
-            pb = pb2;
-            mb = mb2;
         }
-        return true;
-    });
-    w[OFF + 1] = f_add(hj1, f_add(acc0, acc1));
+        if (elim) mus[myrow - J0] = mu;
+        tc.sync();
+        HT_MARK(10);
+        const cd hj1 = f_cms(w[OFF + 1], mu, pr[OFF + 1]);
+        cd acc0 = mk(0.0, 0.0), acc1 = mk(0.0, 0.0);
+        // pairs of columns under one uniform guard; the next pair's broadcasts are
+        // loaded before the current pair's multiply-adds (software pipelining across
+        // the guard; the padded buffers make the over-read harmless)
+        static_assert(kGroup == 2, "the pipelined sweep is written for pairs");
+        cd pa = pr[OFF + 2], ma = mus[OFF + 2], pb = pr[OFF + 3], mb = mus[OFF + 3];
+        static_for<OFF + 2, S, 2>([&](auto gg) {
+            constexpr int c = decltype(gg)::value;
+            if (c < live) {
+                const cd pa2 = pr[c + 2], ma2 = mus[c + 2], pb2 = pr[c + 3], mb2 = mus[c + 3];
+                w[c] = f_cms(w[c], mu, pa);
+                acc0 = f_cma(acc0, ma, w[c]);
+                if constexpr (c + 1 < S) {
+                    w[c + 1] = f_cms(w[c + 1], mu, pb);
+                    acc1 = f_cma(acc1, mb, w[c + 1]);
+                }
+                pa = pa2;
+                ma = ma2;
+                pb = pb2;
+                mb = mb2;
+            }
+            return true;
+        });
+        w[OFF + 1] = f_add(hj1, f_add(acc0, acc1));
+    }
     HT_MARK(11);
 }
 

@@ -33,24 +33,27 @@ int main(int argc, char** argv) {
     cudaMemcpy(d_base, base, 8, cudaMemcpyHostToDevice);
     cudaMemcpy(d_binom, B, sizeof(B), cudaMemcpyHostToDevice);
     ClassItems ci{d_binom, d_seg, d_pre, d_base, 1, m, D, prefix[1], prefix[1], 0, 0, 0, nullptr, nullptr};
-    constexpr int W = TeamWidth<HAFB_S>::W, TPB = kFastThreads / W;
+    #ifndef NTV
+#define NTV kFastThreads
+#endif
+    constexpr int W = TeamWidth<HAFB_S>::W, TPB = NTV / W;
 #ifndef SHV
 #define SHV true
 #endif
     size_t smem = (size_t)TPB * FastLayout<HAFB_S, SHV, false>::TOTAL * sizeof(cd) + (kDMax + 1) * 8;
-    auto k = fast_term_kernel<HAFB_S, false, SHV>;
+    auto k = fast_term_kernel<HAFB_S, false, SHV, NTV>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int occ; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kFastThreads, smem);
+    int occ; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NTV, smem);
     int grid = 148 * occ;
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-    k<<<grid, kFastThreads, smem>>>(d_at, d_dg, D, ci, d_t, d_s);
+    k<<<grid, NTV, smem>>>(d_at, d_dg, D, ci, d_t, d_s);
     cudaDeviceSynchronize();
 #ifdef HAFB_TIMING
     unsigned long long z[16] = {0};
     cudaMemcpyToSymbol(g_phase, z, sizeof(z)); cudaMemcpyToSymbol(g_phase_cnt, z, sizeof(z));
 #endif
     cudaEventRecord(e0);
-    k<<<grid, kFastThreads, smem>>>(d_at, d_dg, D, ci, d_t, d_s);
+    k<<<grid, NTV, smem>>>(d_at, d_dg, D, ci, d_t, d_s);
     cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     unsigned long long ph[16] = {0}, pc[16] = {0};

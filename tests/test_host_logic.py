@@ -130,3 +130,39 @@ def test_no_cpu_fallback_without_device():
 
     with pytest.raises(DeviceError):
         engine.hafnian(workloads.cfg0(n=4))
+
+
+def test_multi_device_plans_with_mocked_devices(monkeypatch):
+    """hafnian(..., devices=N) host logic with the per-device range-list call replaced
+    by the CPU oracle: the deterministic path reassembles the partials in range order
+    (bit-identical to the single-device oracle result for every N); the fast path sums
+    per device and agrees to rounding."""
+    from oracle import oracle as O
+    from paper_1805_12498_b200 import kernels
+
+    def fake_range_list(atilde, diag, n_half, n_ranges, ranges, backend, loops, cap=30, *,
+                        arith=None, device=None):
+        total = 1 << n_half
+        width = -(-(total - 1) // n_ranges)
+        sums, fails = [], []
+        for r in ranges:
+            a = min(1 + int(r) * width, total)
+            b = min(a + width, total)
+            s, f = O.sum_mask_range(atilde, diag, n_half, a, b, 1, backend, loops, cap)
+            sums.append(s[0])
+            fails.append(f[0])
+        return np.array(sums, np.complex128), np.array(fails, np.int64)
+
+    monkeypatch.setattr(kernels, "sum_range_list", fake_range_list)
+    O.build()
+    A = workloads.cfg0()
+    want, _ = O.hafnian(A, backend=1)
+    for n_dev in (1, 2, 3, 8):
+        if n_dev == 1:
+            continue  # the single-device path calls sum_subsets_det, not the mock
+        got = engine.hafnian(A, backend="charpoly", devices=n_dev)
+        assert got == want, n_dev
+        fast = engine.hafnian(A, backend="charpoly", devices=n_dev, reduction="fast")
+        assert abs(fast - want) <= 1e-12 * abs(want), n_dev
+    lw, _ = O.hafnian(workloads.cfg2(n=12), backend=1, include_loops=True)
+    assert engine.loop_hafnian(workloads.cfg2(n=12), backend="charpoly", devices=3) == lw

@@ -77,4 +77,45 @@ __device__ __forceinline__ ItemRef resolve_item(const ClassItems& ci, long long 
     return r;
 }
 
+// Sequential walk over consecutive items of a class.  Inside one segment of one
+// problem, class rank rho+1 is the next larger integer of popcount m (colex order),
+// obtained from the current mask by Gosper's step; the full unranking (a chain of
+// ~D dependent table loads) runs only at the first item and at segment/problem edges.
+struct ItemCursor {
+    long long next = -1;      // the item that continues the walk
+    long long item_end = -1;  // first item outside the current segment (or problem)
+    long long delta = 0;      // out - mask inside the current segment
+    ItemRef ref;
+};
+
+__device__ __forceinline__ uint32_t next_same_popcount(uint32_t x) {
+    const uint32_t c = x & (0u - x);
+    const uint32_t r = x + c;
+    return (((r ^ x) >> 2) >> (__ffs(x) - 1)) | r;
+}
+
+__device__ __forceinline__ ItemRef cursor_item(const ClassItems& ci, long long item, ItemCursor& cur) {
+    if (!ci.mlist && item == cur.next && item < cur.item_end) {
+        cur.next = item + 1;
+        cur.ref.mask = next_same_popcount(cur.ref.mask);
+        cur.ref.out = (long long)cur.ref.mask + cur.delta;
+        return cur.ref;
+    }
+    cur.next = item + 1;
+    cur.ref = resolve_item(ci, item);
+    if (!ci.mlist) {
+        const long long p0 = cur.ref.problem * ci.per_problem;
+        const long long rho = item - p0;
+        int lo = 0, hi = ci.nseg - 1;
+        while (lo < hi) {
+            int mid = (lo + hi + 1) >> 1;
+            if (ci.prefix[mid] <= rho) lo = mid;
+            else hi = mid - 1;
+        }
+        cur.item_end = p0 + ci.prefix[lo + 1];
+        cur.delta = cur.ref.out - (long long)cur.ref.mask;
+    }
+    return cur.ref;
+}
+
 }  // namespace hafb

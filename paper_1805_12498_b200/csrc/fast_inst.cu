@@ -16,7 +16,7 @@ namespace hafb {
 #ifndef HAFB_SMEM_HI
 #define HAFB_SMEM_HI 34
 #endif
-constexpr bool smem_hess(int S) { return (S >= 18 && S <= 24) || S >= HAFB_SMEM_HI; }
+constexpr bool smem_hess(int S) { return !x2_variant(S) && ((S >= 18 && S <= 24) || S >= HAFB_SMEM_HI); }
 
 // Threads per block.  The register-window kernel for 26 <= S <= 32 runs ONE block of
 // 384 threads per SM whose teams are phase-synchronised (__syncthreads between the
@@ -28,7 +28,7 @@ constexpr bool smem_hess(int S) { return (S >= 18 && S <= 24) || S >= HAFB_SMEM_
 #define HAFB_REG_THREADS 384
 #endif
 constexpr int threads_for(int S) {
-    return !smem_hess(S) && S >= 26 ? (S > 32 ? 256 : HAFB_REG_THREADS)
+    return !smem_hess(S) && (S >= 26 || x2_variant(S)) ? (S > 32 ? 256 : HAFB_REG_THREADS)
            : S > 32 ? 64  // 64-lane teams: one team per block (register-limited: 5 teams/SM, not 4)
            : smem_hess(S) ? 32  // one team per block: the register file packs one more team
            : kFastThreads;
@@ -41,7 +41,15 @@ static cudaError_t launch_one(const cd* at, const cd* dg, int n_half, const Clas
     constexpr int NT = threads_for(S);
     constexpr int TPB = NT / W;
     constexpr bool SH = smem_hess(S);
-    const size_t smem = (size_t)TPB * FastLayout<S, SH, L>::TOTAL * sizeof(cd) + (kDMax + 1) * sizeof(double);
+    const size_t base_smem = (size_t)TPB * FastLayout<S, SH, L, !SH && x2_variant(S)>::TOTAL * sizeof(cd) + (kDMax + 1) * sizeof(double);
+    // the one-block-per-SM register classes stage Atilde in shared memory when it fits
+    const int n = 2 * n_half;
+    const size_t a_bytes = (size_t)n * (n + 1) * sizeof(cd);
+    int optin = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const int stage = (NT > kFastThreads && !SH && base_smem + a_bytes <= (size_t)optin) ? 1 : 0;
+    const size_t smem = base_smem + (stage ? a_bytes : 0);
     auto kern = fast_term_kernel<S, L, SH, NT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -51,7 +59,7 @@ static cudaError_t launch_one(const cd* at, const cd* dg, int n_half, const Clas
     const long long want = (ci.n_items + TPB - 1) / TPB;
     const long long cap_blocks = (long long)sms * std::max(occ, 1);
     const int grid = (int)std::max<long long>(1, std::min(want, cap_blocks));
-    kern<<<grid, NT, smem, st>>>(at, dg, n_half, ci, terms, status);
+    kern<<<grid, NT, smem, st>>>(at, dg, n_half, ci, terms, status, stage);
     return cudaGetLastError();
 }
 

@@ -67,6 +67,14 @@ struct TeamWidth {
 };
 
 constexpr int kFastThreads = 128;
+// sizes whose Hessenberg runs in the two-rows-per-lane X2 layout (x2_hessenberg)
+#ifndef HAFB_X2_LO
+#define HAFB_X2_LO 99
+#endif
+#ifndef HAFB_X2_HI
+#define HAFB_X2_HI 32
+#endif
+constexpr bool x2_variant(int S) { return S >= HAFB_X2_LO && S <= HAFB_X2_HI && S <= 32; }
 constexpr int kGroup = 2;
 // threshold partial pivoting: the natural pivot is kept when |h[J+1][J]| >= tau * max
 // (|multipliers| <= 1/tau); 1.0 = classic partial pivoting
@@ -78,18 +86,37 @@ constexpr int kDMax = 31;
 #ifndef HAFB_SHFL_PIVOT
 #define HAFB_SHFL_PIVOT 1
 #endif
+// static-column ("no shift") Hessenberg for the register classes (ns_hessenberg)
+#ifndef HAFB_NS
+#define HAFB_NS 1
+#endif
+#ifndef HAFB_NS_LO
+#define HAFB_NS_LO 26
+#endif
+#ifndef NS_SPECINV
+#define NS_SPECINV 1
+#endif
+#ifndef NS_HIKEY
+#define NS_HIKEY 1
+#endif
+#ifndef NS_PUBPRED
+#define NS_PUBPRED 0
+#endif
+constexpr bool ns_variant(int S) { return HAFB_NS && S >= HAFB_NS_LO && S <= 32; }
 
 // packed upper-Hessenberg storage, column-major: column c holds rows 0..min(c+1, S-1)
 // and starts at c(c+3)/2.
 __host__ __device__ constexpr int hs_elems(int S) { return (S - 1) * (S + 2) / 2 + S; }
 
-template <int S, bool SH = false, bool LOOPS = true>
+template <int S, bool SH = false, bool LOOPS = true, bool X2 = false>
 struct FastLayout {
     static constexpr int HS = 0;                      // packed Hessenberg, or (SH) the S x S matrix
     static constexpr int SP = S + 12;                  // padded pivot-row / multiplier length
     static constexpr int PR = HS + (SH ? S * S : hs_elems(S));  // [2][SP] pivot rows (register variant)
-    static constexpr int MU = PR + (SH ? 0 : 2 * SP);  // [2][SP] multipliers
-    static constexpr int CF = MU + 2 * SP;            // [2][S] charpoly coefs
+    // [2][SP] multipliers (the register variant for S >= 26 shuffles the pivot row: no PR);
+    // X2: [2][S][2] interleaved (pivot-row entry, multiplier) per logical column
+    static constexpr int MU = PR + ((SH || X2 || (HAFB_SHFL_PIVOT && S >= 26 && !HAFB_NS)) ? 0 : 2 * SP);
+    static constexpr int CF = MU + (X2 ? 4 * S : 2 * SP);  // [2][S] charpoly coefs
     static constexpr int RED = CF + 2 * S;            // [2][2][2] argmax exchange (W = 64)
     static constexpr int A = RED + 8;                 // [S+1] charpoly coefficients
     static constexpr int U = A + S + 1;               // [2][S] loop-chain vector (LOOPS)
@@ -283,6 +310,9 @@ __device__ __forceinline__ void fast_hess_step(cd (&w)[S], const int J0, int& my
         p = r[0];
         brow = (int)r[1].re;
     }
+    // the reciprocal's dependent DFMA chain is issued before the relabel and the column
+    // swap's branch tree, which then run under its latency
+    const cd ip = f_inv(p);
     HT_MARK(5);
     HT_MARK(13);
     if (myrow == brow) myrow = J + 1;
@@ -291,7 +321,6 @@ __device__ __forceinline__ void fast_hess_step(cd (&w)[S], const int J0, int& my
     HT_MARK(6);
     if (brow != J + 1) swap_bs<S, OFF + 2, S>(w, OFF + 1, brow - J0);
     HT_MARK(9);
-    const cd ip = f_inv(p);
     const bool elim = myrow >= J + 2 && myrow < S;
     const cd mu = elim ? f_mul(hj, ip) : mk(0.0, 0.0);
     HT_MARK(7);
@@ -523,12 +552,402 @@ __device__ __forceinline__ void smem_hessenberg(cd* H, int& myrow, const TeamCtx
     tc.sync();
 }
 
+
+
+// ============================================================================ NS variant
+// Hessenberg reduction (_numba.py:36-67) with the lane's row at STATIC column indices
+// and no register window: the sweep of step J runs from column S-1 DOWN to J+2 and
+// leaves at J+2, so dead columns cost nothing; columns J (the pivot column) and J+1
+// travel in registers (hj, hn) from one step to the next, so the only dynamic register
+// index left is the pivot column swap (one read-modify-write branch tree).  The window
+// version moved every live register two places every second step (IMAD.MOV / FSEL:
+// ~20 % of the issued instructions at S = 28).  The pivot row is published to shared
+// memory by its lane (a broadcast LDS.128 per column instead of four 32-bit shuffles).
+// Same exact-arithmetic identities as fast_hessenberg; the gemv sums the columns in
+// descending order.
+
+// t = w[b]; w[b] = v  (team-uniform runtime b in [LO, HI))
+template <int S, int LO, int HI>
+__device__ __forceinline__ void ns_xchg(cd (&w)[S], int b, cd& v) {
+    if constexpr (HI - LO == 1) {
+        const cd t = w[LO];
+        vmov(w[LO].re, v.re);
+        vmov(w[LO].im, v.im);
+        vmov(v.re, t.re);
+        vmov(v.im, t.im);
+    } else if constexpr (HI > LO) {
+        constexpr int MID = (LO + HI) / 2;
+        if (b < MID) ns_xchg<S, LO, MID>(w, b, v);
+        else ns_xchg<S, MID, HI>(w, b, v);
+    }
+}
+// v = w[b]
+template <int S, int LO, int HI>
+__device__ __forceinline__ void ns_read(const cd (&w)[S], int b, cd& v) {
+    if constexpr (HI - LO == 1) {
+        v = w[LO];
+    } else if constexpr (HI > LO) {
+        constexpr int MID = (LO + HI) / 2;
+        if (b < MID) ns_read<S, LO, MID>(w, b, v);
+        else ns_read<S, MID, HI>(w, b, v);
+    }
+}
+
+template <int S, int W>
+__device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const TeamCtx<W>& tc, cd* ws) {
+    static_assert(W == 32, "NS variant: one warp per subset");
+    using L = FastLayout<S>;
+    cd* Hs = ws + L::HS;
+    cd* pr = ws + L::PR;  // pivot row, by logical column
+    cd* mus = ws + L::MU;  // multiplier of each logical row
+    const int lane = tc.lane;
+    cd hj = w[0], hn = w[1];
+#pragma unroll 1
+    for (int J = 0; J < S - 2; ++J) {
+        const double key = (myrow > J && myrow < S) ? fabs(hj.re) + fabs(hj.im) : 0.0;
+#if NS_SPECINV
+        // every candidate inverts its own entry while the argmax is in flight; the
+        // winner's reciprocal travels with its value (the inverse leaves the serial chain)
+        const cd myinv = f_inv(hj);
+#endif
+#if NS_HIKEY
+        // argmax on the high word of the nonnegative double key (monotone in the key),
+        // low 6 bits replaced by (63 - lane): larger key wins, ties -> lowest lane
+        const unsigned kb = (unsigned)__double2hiint(key);
+#else
+        const unsigned kb = key > 0.0 ? __float_as_uint(__double2float_ru(key)) : 0u;
+#endif
+        const unsigned mx = __reduce_max_sync(0xffffffffu, (kb & ~63u) | (unsigned)(63 - lane));
+        const int wl = 63 - (int)(mx & 63u);
+        const int CS = (J * (J + 3)) / 2;  // column J in the packed store
+        if ((mx & ~63u) == 0u) {  // nothing to eliminate below the subdiagonal: no update
+            if (myrow <= J + 1) Hs[CS + myrow] = hj;
+            hj = hn;
+            ns_read<S, 2, S>(w, J + 2, hn);
+            continue;
+        }
+        const int brow = __shfl_sync(0xffffffffu, myrow, wl);
+#if NS_SPECINV
+        cd ip;
+        ip.re = __shfl_sync(0xffffffffu, myinv.re, wl);
+        ip.im = __shfl_sync(0xffffffffu, myinv.im, wl);
+#else
+        cd p;
+        p.re = __shfl_sync(0xffffffffu, hj.re, wl);
+        p.im = __shfl_sync(0xffffffffu, hj.im, wl);
+        const cd ip = f_inv(p);
+#endif
+        if (myrow == brow) myrow = J + 1;
+        else if (myrow == J + 1) myrow = brow;
+        const bool elim = myrow >= J + 2 && myrow < S;
+        const cd mu = elim ? f_mul(hj, ip) : mk(0.0, 0.0);
+        if (myrow < S) mus[myrow] = mu;
+        if (myrow <= J + 1) Hs[CS + myrow] = hj;
+        // column swap J+1 <-> brow: column J+1 is hn, column brow >= J+2 sits at w[brow]
+        if (brow != J + 1) ns_xchg<S, 2, S>(w, brow, hn);
+        // publish the pivot row (logical row J+1): predicated stores, no per-column branch
+        const bool pl = lane == wl;
+#if NS_PUBPRED
+        if (pl) pr[J + 1] = hn;
+        static_for<2, S>([&](auto cc) {
+            constexpr int c = decltype(cc)::value;
+            if (pl) pr[c] = w[c];
+            return true;
+        });
+#else
+        if (pl) {
+            pr[J + 1] = hn;
+            static_for<0, S - 2>([&](auto ii) {
+                constexpr int c = S - 1 - decltype(ii)::value;
+                if (c < J + 2) return false;
+                pr[c] = w[c];
+                return true;
+            });
+        }
+#endif
+        __syncwarp();
+        // sweep, columns S-1 down to J+2: row update fused with the column gemv; at J+2
+        // stash the next step's column J+2 and finish column J+1 (the gemv target)
+        cd acc0 = mk(0.0, 0.0), acc1 = mk(0.0, 0.0);
+        cd pa = pr[S - 1], ma = mus[S - 1];
+        static_for<0, S - 2>([&](auto ii) {
+            constexpr int c = S - 1 - decltype(ii)::value;
+            const cd pn = pr[c - 1], mn = mus[c - 1];  // next column's broadcasts (c-1 >= 1)
+            w[c] = f_cms(w[c], mu, pa);
+            if constexpr (c & 1) acc1 = f_cma(acc1, ma, w[c]);
+            else acc0 = f_cma(acc0, ma, w[c]);
+            pa = pn;
+            ma = mn;
+            if (c == J + 2) {
+                const cd nh = w[c];
+                hj = f_add(f_cms(hn, mu, pa), f_add(acc0, acc1));  // pa = pr[J+1]
+                hn = nh;
+                return false;
+            }
+            return true;
+        });
+    }
+    // logical columns S-2 (hj) and S-1 (hn): every row
+    if (myrow < S) {
+        Hs[((S - 2) * (S + 1)) / 2 + myrow] = hj;
+        Hs[((S - 1) * (S + 2)) / 2 + myrow] = hn;
+    }
+}
+
+// ============================================================================ X2 layout
+// Hessenberg reduction with each lane holding TWO rows and HALF of the columns
+// (column-cyclic): lane = 2g + h owns physical rows 2g, 2g+1 (slots 0, 1) and the
+// columns c = 2k + h.  Every broadcast operand of the sweep (the pivot-row entry of
+// column c and the multiplier of logical row c) then feeds 16 DFMA (two rows) instead
+// of 8, which halves the shared-memory / shuffle traffic per DFMA -- on B200 a
+// warp-wide broadcast LDS.128 issues at ~0.5/clk/SM and SHFL at ~1/clk/SM against
+// ~1.8 warp-DFMA/clk/SM (tools/micro/shfl.cu), so the one-row-per-lane sweep was
+// bound by its broadcasts.  The two halves of a row meet in one shfl.xor per step
+// (the column gemv's partial sums).  Same arithmetic identities as fast_hessenberg;
+// window positions k of a half hold columns 2(k0 + k) + h after k0 = J0/2 shifts.
+template <int S>
+__device__ __forceinline__ cd x2_shfl_xor1(cd v) {
+    cd r;
+    r.re = __shfl_xor_sync(0xffffffffu, v.re, 1);
+    r.im = __shfl_xor_sync(0xffffffffu, v.im, 1);
+    return r;
+}
+
+// v_s = w[s][pb] / w[s][pb] = v_s (if en) for a team-uniform runtime pb in [LO, HI)
+template <int S, int LO, int HI>
+__device__ __forceinline__ void x2_read(const cd (&w)[2][S / 2], int pb, cd& v0, cd& v1) {
+    if constexpr (HI - LO == 1) {
+        v0 = w[0][LO];
+        v1 = w[1][LO];
+    } else if constexpr (HI > LO) {
+        constexpr int MID = (LO + HI) / 2;
+        if (pb < MID) x2_read<S, LO, MID>(w, pb, v0, v1);
+        else x2_read<S, MID, HI>(w, pb, v0, v1);
+    }
+}
+template <int S, int LO, int HI>
+__device__ __forceinline__ void x2_write(cd (&w)[2][S / 2], int pb, bool en, const cd& v0, const cd& v1) {
+    if constexpr (HI - LO == 1) {
+        if (en) {
+            w[0][LO] = v0;
+            w[1][LO] = v1;
+        }
+    } else if constexpr (HI > LO) {
+        constexpr int MID = (LO + HI) / 2;
+        if (pb < MID) x2_write<S, LO, MID>(w, pb, en, v0, v1);
+        else x2_write<S, MID, HI>(w, pb, en, v0, v1);
+    }
+}
+
+// swap logical columns J+1 (half HA, window position PA) and brow (half b, position pb)
+template <int S, int HA, int PA>
+__device__ __forceinline__ void x2_colswap(cd (&w)[2][S / 2], int pb, bool same, int h) {
+    constexpr int KW = S / 2;
+    const bool ha = h == HA;
+    cd v0, v1;
+    x2_read<S, PA, KW>(w, pb, v0, v1);
+    const cd a0 = w[0][PA], a1 = w[1][PA];
+    cd n0, n1;  // new values of position pb
+    if (same) {
+        n0 = a0;
+        n1 = a1;
+    } else {
+        // the partner lane (other half, same rows) holds the other column
+        const cd o0 = ha ? a0 : v0, o1 = ha ? a1 : v1;
+        n0 = x2_shfl_xor1<S>(o0);
+        n1 = x2_shfl_xor1<S>(o1);
+        v0 = n0;
+        v1 = n1;
+    }
+    // half HA: position PA <- column brow (own if same, else the partner's);
+    // position pb <- column J+1: own (same, half HA) or the partner's (!same, half b)
+    if (ha) {
+        w[0][PA] = v0;
+        w[1][PA] = v1;
+    }
+    x2_write<S, PA, KW>(w, pb, same ? ha : !ha, n0, n1);
+}
+
+// One step J = J0 + OFF (OFF = 0..3) of the reduction on the X2 window: at the group
+// start J0 (a multiple of 2), position k of half h holds logical column 2(k0 + k) + h.
+template <int S, int OFF, bool LOOPS>
+__device__ __forceinline__ void x2_step(cd (&w)[2][S / 2], int (&lr)[2], const int J0,
+                                        const TeamCtx<32>& tc, cd* ws) {
+    using L = FastLayout<S, false, LOOPS, true>;
+    constexpr int KW = S / 2;
+    constexpr int HJ = OFF & 1, PJ = OFF >> 1;              // column J: half, position
+    constexpr int HA = (OFF + 1) & 1, PA = (OFF + 1) >> 1;  // column J+1
+    const int J = J0 + OFF;
+    const int k0 = J0 >> 1;
+    const int live = KW - k0;  // live window positions per half
+    const int lane = tc.lane, g = lane >> 1, h = lane & 1;
+    cd* Hs = ws + L::HS;
+    cd* X = ws + L::MU + (OFF & 1) * 2 * S;  // X[2c] = pivot-row entry, X[2c+1] = multiplier of row c
+    // ---- pivot search over column J; ties -> lowest physical row
+    unsigned pk = 0;
+    if (h == HJ) {
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            const cd v = w[s][PJ];
+            const double key = (lr[s] > J && lr[s] < S) ? fabs(v.re) + fabs(v.im) : 0.0;
+            const unsigned kb = key > 0.0 ? __float_as_uint(__double2float_ru(key)) : 0u;
+            const unsigned pc = (kb & ~63u) | (unsigned)(63 - (2 * g + s));
+            pk = pc > pk ? pc : pk;
+        }
+    }
+    const unsigned mx = __reduce_max_sync(0xffffffffu, pk);
+    const int CS = (J * (J + 3)) / 2;  // column J in the packed store
+    if ((mx & ~63u) == 0u) {  // nothing to eliminate below the subdiagonal
+        if (h == HJ) {
+#pragma unroll
+            for (int s = 0; s < 2; ++s)
+                if (lr[s] <= J + 1) Hs[CS + lr[s]] = w[s][PJ];
+        }
+        return;
+    }
+    const int pw = 63 - (int)(mx & 63u);  // physical pivot row
+    const int ps = pw & 1;
+    const int src = (pw >> 1) * 2 + HJ;
+    const cd mine = ps ? w[1][PJ] : w[0][PJ];
+    const int mylab = ps ? lr[1] : lr[0];
+    cd p;
+    p.re = __shfl_sync(0xffffffffu, mine.re, src);
+    p.im = __shfl_sync(0xffffffffu, mine.im, src);
+    const int brow = __shfl_sync(0xffffffffu, mylab, src);
+    const cd ip = f_inv(p);
+    // ---- row swap J+1 <-> brow as a relabelling
+#pragma unroll
+    for (int s = 0; s < 2; ++s) lr[s] = lr[s] == brow ? J + 1 : (lr[s] == J + 1 ? brow : lr[s]);
+    if (h == HJ) {
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+            if (lr[s] <= J + 1) Hs[CS + lr[s]] = w[s][PJ];
+    }
+    // ---- column swap J+1 <-> brow
+    if (brow != J + 1) {
+        const int b = brow & 1;
+        const int pb = ((brow - b) >> 1) - k0;
+        x2_colswap<S, HA, PA>(w, pb, b == HA, h);
+    }
+    // ---- multipliers (half HJ holds column J) and the pivot row, published per logical column
+    cd mu[2];
+    if (h == HJ) {
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            const bool elim = lr[s] >= J + 2 && lr[s] < S;
+            mu[s] = elim ? f_mul(w[s][PJ], ip) : mk(0.0, 0.0);
+            if (lr[s] < S) X[2 * lr[s] + 1] = mu[s];
+        }
+    }
+    {
+        // the two lanes holding the pivot row store its entries; the slot choice is
+        // warp-uniform, the lane predicate is applied per store (no divergent branch)
+        const bool pl = g == (pw >> 1);
+        cd* Xp = X + 2 * (2 * k0 + h);
+        if (ps) {
+            static_for<PJ, KW>([&](auto kk) {
+                constexpr int k = decltype(kk)::value;
+                if (k < live) {
+                    if (pl) Xp[4 * k] = w[1][k];
+                }
+                return true;
+            });
+        } else {
+            static_for<PJ, KW>([&](auto kk) {
+                constexpr int k = decltype(kk)::value;
+                if (k < live) {
+                    if (pl) Xp[4 * k] = w[0][k];
+                }
+                return true;
+            });
+        }
+    }
+    __syncwarp();
+    if (h != HJ) {
+#pragma unroll
+        for (int s = 0; s < 2; ++s) mu[s] = lr[s] < S ? X[2 * lr[s] + 1] : mk(0.0, 0.0);
+    }
+    // ---- sweep: rank-1 row update fused with the column gemv.  Positions from PJ on
+    //      cover every column >= J+1; the few columns <= J it also touches are final
+    //      (stored) and have zero multipliers, so they add nothing to the gemv.
+    cd acc0 = mk(0.0, 0.0), acc1 = mk(0.0, 0.0);
+    const cd* Xh = X + 2 * (2 * k0 + h);
+    static_for<PJ, KW>([&](auto kk) {
+        constexpr int k = decltype(kk)::value;
+        if (k < live) {
+            const cd pc = Xh[4 * k], mc = Xh[4 * k + 1];
+            w[0][k] = f_cms(w[0][k], mu[0], pc);
+            w[1][k] = f_cms(w[1][k], mu[1], pc);
+            acc0 = f_cma(acc0, mc, w[0][k]);
+            acc1 = f_cma(acc1, mc, w[1][k]);
+        }
+        return true;
+    });
+    const cd t0 = x2_shfl_xor1<S>(acc0), t1 = x2_shfl_xor1<S>(acc1);
+    if (h == HA) {  // column J+1
+        w[0][PA] = f_add(w[0][PA], f_add(acc0, t0));
+        w[1][PA] = f_add(w[1][PA], f_add(acc1, t1));
+    }
+}
+
+#ifndef HAFB_X2_GROUP
+#define HAFB_X2_GROUP 4
+#endif
+
+template <int S, int NSH>
+__device__ __forceinline__ void x2_shift(cd (&w)[2][S / 2]) {
+    // shift the window by NSH columns per half (dead positions shift too: plain moves)
+    static_for<0, S / 2 - NSH>([&](auto kk) {
+        constexpr int k = decltype(kk)::value;
+        w[0][k] = w[0][k + NSH];
+        w[1][k] = w[1][k + NSH];
+        return true;
+    });
+}
+
+template <int S, bool LOOPS>
+__device__ __forceinline__ void x2_hessenberg(cd (&w)[2][S / 2], int (&lr)[2], const TeamCtx<32>& tc,
+                                              cd* ws) {
+    using L = FastLayout<S, false, LOOPS, true>;
+    int J0 = 0;
+    if constexpr (HAFB_X2_GROUP == 4) {
+        // groups of four steps per window shift of two (half the register moves)
+#pragma unroll 1
+        for (; J0 + 4 <= S - 2; J0 += 4) {
+            x2_step<S, 0, LOOPS>(w, lr, J0, tc, ws);
+            x2_step<S, 1, LOOPS>(w, lr, J0, tc, ws);
+            x2_step<S, 2, LOOPS>(w, lr, J0, tc, ws);
+            x2_step<S, 3, LOOPS>(w, lr, J0, tc, ws);
+            x2_shift<S, 2>(w);
+        }
+        if (J0 < S - 2) {  // S - 2 = 2 (mod 4): one pair left
+            x2_step<S, 0, LOOPS>(w, lr, J0, tc, ws);
+            x2_step<S, 1, LOOPS>(w, lr, J0, tc, ws);
+            x2_shift<S, 1>(w);
+        }
+    } else {
+#pragma unroll 1
+        for (; J0 < S - 2; J0 += 2) {
+            x2_step<S, 0, LOOPS>(w, lr, J0, tc, ws);
+            x2_step<S, 1, LOOPS>(w, lr, J0, tc, ws);
+            x2_shift<S, 1>(w);
+        }
+    }
+    // logical columns S-2 (half 0) and S-1 (half 1) are at window position 0
+    cd* Hs = ws + L::HS;
+    const int c = S - 2 + (tc.lane & 1);
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+        if (lr[s] < S) Hs[(c * (c + 3)) / 2 + lr[s]] = w[s][0];
+}
+
 template <int S, bool LOOPS, bool SH, int NT = kFastThreads>
 __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ atilde,
                                                                  const cd* __restrict__ diag,
                                                                  int n_half, ClassItems ci,
                                                                  cd* __restrict__ terms,
-                                                                 int8_t* __restrict__ status) {
+                                                                 int8_t* __restrict__ status,
+                                                                 int stage_a) {
     constexpr int W = TeamWidth<S>::W;
     constexpr int TPB = NT / W;
     constexpr int M = S / 2;
@@ -536,7 +955,8 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
     // blocks of more than 128 threads (one block per SM) keep their teams in the same
     // phase so the SM's instruction cache holds one phase's code at a time
     constexpr bool PSYNC = NT > kFastThreads;
-    using L = FastLayout<S, SH, LOOPS>;
+    constexpr bool X2 = !SH && x2_variant(S);
+    using L = FastLayout<S, SH, LOOPS, X2>;
     extern __shared__ cd smem[];
     TeamCtx<W> tc;
     tc.tib = threadIdx.x / W;
@@ -552,21 +972,46 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
     // reciprocals 1/k for the exp recurrence (block-shared, written once)
     double* INV = reinterpret_cast<double*>(smem + (size_t)TPB * L::TOTAL);
     for (int k = threadIdx.x; k <= kDMax; k += blockDim.x) INV[k] = k ? 1.0 / k : 0.0;
-    __syncthreads();
     const int n = 2 * n_half;
     const int D = n_half;
-    const long long stride = (long long)gridDim.x * TPB;
+    // each team walks a contiguous run of the class's items (successive masks by
+    // Gosper's step, ItemCursor); every team runs the same trip count (block-uniform
+    // loop for the phase barriers)
+    const long long n_teams = (long long)gridDim.x * TPB;
+    const long long chunk = (ci.n_items + n_teams - 1) / n_teams;
+    const long long first = ((long long)blockIdx.x * TPB + tc.tib) * chunk;
+    // Atilde staged in shared memory (row stride n+1: the lanes' rows fall in distinct
+    // banks) for the block's first problem; the subset gathers then read shared memory
+    // instead of issuing S scattered global loads per lane
+    cd* As = reinterpret_cast<cd*>(INV + kDMax + 1);
+    const int ldA = n + 1;
+    long long staged_problem = -1;
+    if (stage_a) {
+        staged_problem = ((long long)blockIdx.x * TPB * chunk) / ci.per_problem;
+        const cd* src = atilde + staged_problem * ci.at_stride;
+        for (int i = threadIdx.x; i < n * n; i += blockDim.x) As[(i / n) * ldA + (i % n)] = src[i];
+    }
+    __syncthreads();
+    ItemCursor cur;
 #ifdef HAFB_STAGGER
     // experiment: de-phase the warps of an SM so their serial sections overlap others' sweeps
     __nanosleep((unsigned)(((threadIdx.x >> 5) + 4 * (blockIdx.x % 4)) % 16) * HAFB_STAGGER);
 #endif
 
-    for (long long base = (long long)blockIdx.x * TPB; base < ci.n_items; base += stride) {
+    for (long long it = 0; it < chunk; ++it) {
         HT_DECL
-        const long long item = base + tc.tib;
+        const long long item = first + it;
         const bool valid = item < ci.n_items;
-        const ItemRef ir = resolve_item(ci, valid ? item : base);
+        const ItemRef ir = cursor_item(ci, valid ? item : 0, cur);
+        const bool from_smem = ir.problem == staged_problem;
         const cd* at = atilde + ir.problem * ci.at_stride;
+        // row-major Atilde entry (r, c) gathered from the staged copy or from global
+        // memory (team-uniform choice; each call site is instantiated for both spaces
+        // so the loads stay LDS / LDG instead of generic)
+        auto gather = [&](auto&& body) {
+            if (from_smem) body(static_cast<const cd*>(As), ldA);
+            else body(at, n);
+        };
         const cd* dg = diag + ir.problem * ci.dg_stride;
         // vertex list: vertex c = 2*bit[c/2] + (c&1); every index below is static except
         // the lane's own pair, found with __fns (no dynamically indexed local arrays)
@@ -586,10 +1031,12 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
         if constexpr (LOOPS) {
             // lane j holds column j of B: B[i][j] = Atilde[v_{j^1}][v_{i^1}]
             const int rj = 2 * mybit + ((lane & 1) ^ 1);
-            static_for<0, S>([&](auto i) {
-                const int ci1 = 2 * vbit[i() >> 1] + ((i() & 1) ^ 1);
-                hr[i()] = lane < S ? at[rj * n + ci1] : mk(0.0, 0.0);
-                return true;
+            gather([&](const cd* src, int ld) {
+                static_for<0, S>([&](auto i) {
+                    const int ci1 = 2 * vbit[i() >> 1] + ((i() & 1) ^ 1);
+                    hr[i()] = lane < S ? src[rj * ld + ci1] : mk(0.0, 0.0);
+                    return true;
+                });
             });
             cd u = lane < S ? dg[2 * mybit + (lane & 1)] : mk(0.0, 0.0);
             const cd xv = lane < S ? dg[2 * mybit + ((lane & 1) ^ 1)] : mk(0.0, 0.0);
@@ -629,23 +1076,46 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
         int myrow = lane;
         if constexpr (SH) {
             cd* H = ws + L::HS;
-            static_for<0, S>([&](auto c) {
-                const int vc = 2 * vbit[c() >> 1] + (c() & 1);
-                if (lane < S) H[c() * S + lane] = at[vr * n + vc];
-                return true;
+            gather([&](const cd* src, int ld) {
+                static_for<0, S>([&](auto c) {
+                    const int vc = 2 * vbit[c() >> 1] + (c() & 1);
+                    if (lane < S) H[c() * S + lane] = src[vr * ld + vc];
+                    return true;
+                });
             });
             tc.sync();
             HT_MARK(0);
             smem_hessenberg<S, W, LOOPS>(H, myrow, tc, ws);
+        } else if constexpr (X2) {
+            // lane 2g+h: rows 2g, 2g+1 (vertices 2 v_g, 2 v_g + 1), columns 2k+h (vertex 2 v_k + h)
+            constexpr int KW = S / 2;
+            const int g = lane >> 1, h = lane & 1;
+            const int gb = g < M ? (int)__fns(ir.mask, 0, g + 1) : 0;
+            cd w2[2][KW];
+            int lr[2] = {2 * g, 2 * g + 1};
+            gather([&](const cd* src, int ld) {
+                static_for<0, KW>([&](auto kk) {
+                    constexpr int k = decltype(kk)::value;
+                    const int vc = 2 * vbit[k] + h;
+                    w2[0][k] = g < M ? src[(2 * gb) * ld + vc] : mk(0.0, 0.0);
+                    w2[1][k] = g < M ? src[(2 * gb + 1) * ld + vc] : mk(0.0, 0.0);
+                    return true;
+                });
+            });
+            HT_MARK(0);
+            x2_hessenberg<S, LOOPS>(w2, lr, tc, ws);
         } else {
-            static_for<0, S>([&](auto c) {
-                const int vc = 2 * vbit[c() >> 1] + (c() & 1);
-                hr[c()] = lane < S ? at[vr * n + vc] : mk(0.0, 0.0);
-                return true;
+            gather([&](const cd* src, int ld) {
+                static_for<0, S>([&](auto c) {
+                    const int vc = 2 * vbit[c() >> 1] + (c() & 1);
+                    hr[c()] = lane < S ? src[vr * ld + vc] : mk(0.0, 0.0);
+                    return true;
+                });
             });
             HT_MARK(0);
             // ---------------------------------------------- Hessenberg (_numba.py:36-67)
-            fast_hessenberg<S, W>(hr, myrow, tc, ws);
+            if constexpr (ns_variant(S)) ns_hessenberg<S, W>(hr, myrow, tc, ws);
+            else fast_hessenberg<S, W>(hr, myrow, tc, ws);
         }
         HT_MARK(1);
         if constexpr (PSYNC) __syncthreads();

@@ -40,20 +40,21 @@ int main(int argc, char** argv) {
 #ifndef SHV
 #define SHV true
 #endif
-    size_t smem = (size_t)TPB * FastLayout<HAFB_S, SHV, false>::TOTAL * sizeof(cd) + (kDMax + 1) * 8;
+    const int stage = (NTV > kFastThreads && !SHV) ? 1 : 0;
+    size_t smem = (size_t)TPB * FastLayout<HAFB_S, SHV, false, !SHV && x2_variant(HAFB_S)>::TOTAL * sizeof(cd) + (kDMax + 1) * 8 + (stage ? (size_t)n * (n + 1) * sizeof(cd) : 0);
     auto k = fast_term_kernel<HAFB_S, false, SHV, NTV>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int occ; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NTV, smem);
     int grid = 148 * occ;
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-    k<<<grid, NTV, smem>>>(d_at, d_dg, D, ci, d_t, d_s);
+    k<<<grid, NTV, smem>>>(d_at, d_dg, D, ci, d_t, d_s, stage);
     cudaDeviceSynchronize();
 #ifdef HAFB_TIMING
     unsigned long long z[16] = {0};
     cudaMemcpyToSymbol(g_phase, z, sizeof(z)); cudaMemcpyToSymbol(g_phase_cnt, z, sizeof(z));
 #endif
     cudaEventRecord(e0);
-    k<<<grid, NTV, smem>>>(d_at, d_dg, D, ci, d_t, d_s);
+    k<<<grid, NTV, smem>>>(d_at, d_dg, D, ci, d_t, d_s, stage);
     cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     unsigned long long ph[16] = {0}, pc[16] = {0};

@@ -10,25 +10,34 @@
 
 namespace hafb {
 
-// Hessenberg variant per size (measured on B200, tools/class_time.py under ncu): the
-// shared-memory reduction wins for 18 <= S <= 24 and S >= 34 (these classes are
-// shared-memory-bandwidth bound), the register-window reduction elsewhere.
+// Hessenberg variant per size (measured on B200, tools/micro/phase.cu and
+// tools/class_time.py under ncu):
+//   18 <= S <= 32  static-column register reduction (ns_hessenberg, one warp per subset);
+//   S >= 34        shared-memory reduction over 64-lane teams (smem_hessenberg: a two-warp
+//                  static-column team measured 7-11 % slower -- its second warp carries
+//                  2..8 rows but issues the whole instruction stream);
+//   S <= 16        register-window reduction (fast_hessenberg, 16-lane teams).
 #ifndef HAFB_SMEM_HI
 #define HAFB_SMEM_HI 34
 #endif
-constexpr bool smem_hess(int S) { return !x2_variant(S) && ((S >= 18 && S <= 24) || S >= HAFB_SMEM_HI); }
+constexpr bool smem_hess(int S) { return !ns_variant(S) && ((S >= 18 && S <= 24) || S >= HAFB_SMEM_HI); }
 
-// Threads per block.  The register-window kernel for 26 <= S <= 32 runs ONE block of
-// 384 threads per SM whose teams are phase-synchronised (__syncthreads between the
-// Hessenberg, charpoly and series phases): the SM's instruction cache then holds one
-// phase's code at a time, which removed the top stall ("no instruction", 34% of
-// stall cycles at S = 30) and cut these classes by ~20%.  The shared-memory classes
-// are L1-bound and gain nothing from it (measured), so they keep 128-thread blocks.
+// Threads per block.  The register classes run ONE block per SM whose teams are
+// phase-synchronised (__syncthreads between the Hessenberg, charpoly and series phases):
+// the SM's instruction cache then holds one phase's code at a time (this removed the
+// "no instruction" stall, 34% of stall cycles at S = 30), and the block stages Atilde in
+// shared memory for the gathers.  512 threads (16 teams, <= 128 registers) for S <= 22,
+// 384 (12 teams, <= 168 registers) up to S = 32.  The shared-memory classes are L1-bound
+// and gain nothing from phase sync (measured), so they keep small blocks.
+#ifndef HAFB_NS_WIDE_THREADS
+#define HAFB_NS_WIDE_THREADS 64
+#endif
 #ifndef HAFB_REG_THREADS
 #define HAFB_REG_THREADS 384
 #endif
 constexpr int threads_for(int S) {
-    return !smem_hess(S) && (S >= 26 || x2_variant(S)) ? (S > 32 ? 256 : HAFB_REG_THREADS)
+    return ns_variant(S) ? (S > 32 ? HAFB_NS_WIDE_THREADS : S <= 22 ? 512 : HAFB_REG_THREADS)
+           : !smem_hess(S) && S >= 26 ? (S > 32 ? 256 : HAFB_REG_THREADS)
            : S > 32 ? 64  // 64-lane teams: one team per block (register-limited: 5 teams/SM, not 4)
            : smem_hess(S) ? 32  // one team per block: the register file packs one more team
            : kFastThreads;
@@ -41,7 +50,7 @@ static cudaError_t launch_one(const cd* at, const cd* dg, int n_half, const Clas
     constexpr int NT = threads_for(S);
     constexpr int TPB = NT / W;
     constexpr bool SH = smem_hess(S);
-    const size_t base_smem = (size_t)TPB * FastLayout<S, SH, L, !SH && x2_variant(S)>::TOTAL * sizeof(cd) + (kDMax + 1) * sizeof(double);
+    const size_t base_smem = (size_t)TPB * FastLayout<S, SH, L>::TOTAL * sizeof(cd) + (kDMax + 1) * sizeof(double);
     // the one-block-per-SM register classes stage Atilde in shared memory when it fits
     const int n = 2 * n_half;
     const size_t a_bytes = (size_t)n * (n + 1) * sizeof(cd);

@@ -67,14 +67,6 @@ struct TeamWidth {
 };
 
 constexpr int kFastThreads = 128;
-// sizes whose Hessenberg runs in the two-rows-per-lane X2 layout (x2_hessenberg)
-#ifndef HAFB_X2_LO
-#define HAFB_X2_LO 99
-#endif
-#ifndef HAFB_X2_HI
-#define HAFB_X2_HI 32
-#endif
-constexpr bool x2_variant(int S) { return S >= HAFB_X2_LO && S <= HAFB_X2_HI && S <= 32; }
 constexpr int kGroup = 2;
 // threshold partial pivoting: the natural pivot is kept when |h[J+1][J]| >= tau * max
 // (|multipliers| <= 1/tau); 1.0 = classic partial pivoting
@@ -91,7 +83,7 @@ constexpr int kDMax = 31;
 #define HAFB_NS 1
 #endif
 #ifndef HAFB_NS_LO
-#define HAFB_NS_LO 26
+#define HAFB_NS_LO 18
 #endif
 #ifndef NS_SPECINV
 #define NS_SPECINV 1
@@ -99,24 +91,35 @@ constexpr int kDMax = 31;
 #ifndef NS_HIKEY
 #define NS_HIKEY 1
 #endif
+#ifndef NS_PAIR
+#define NS_PAIR 0
+#endif
+#ifndef HAFB_CPRE
+#define HAFB_CPRE 0
+#endif
+#ifndef NS_SHFLROW
+#define NS_SHFLROW 0
+#endif
 #ifndef NS_PUBPRED
 #define NS_PUBPRED 0
 #endif
-constexpr bool ns_variant(int S) { return HAFB_NS && S >= HAFB_NS_LO && S <= 32; }
+#ifndef HAFB_NS_HI
+#define HAFB_NS_HI 32
+#endif
+constexpr bool ns_variant(int S) { return HAFB_NS && S >= HAFB_NS_LO && S <= HAFB_NS_HI; }
 
 // packed upper-Hessenberg storage, column-major: column c holds rows 0..min(c+1, S-1)
 // and starts at c(c+3)/2.
 __host__ __device__ constexpr int hs_elems(int S) { return (S - 1) * (S + 2) / 2 + S; }
 
-template <int S, bool SH = false, bool LOOPS = true, bool X2 = false>
+template <int S, bool SH = false, bool LOOPS = true>
 struct FastLayout {
     static constexpr int HS = 0;                      // packed Hessenberg, or (SH) the S x S matrix
     static constexpr int SP = S + 12;                  // padded pivot-row / multiplier length
     static constexpr int PR = HS + (SH ? S * S : hs_elems(S));  // [2][SP] pivot rows (register variant)
-    // [2][SP] multipliers (the register variant for S >= 26 shuffles the pivot row: no PR);
-    // X2: [2][S][2] interleaved (pivot-row entry, multiplier) per logical column
-    static constexpr int MU = PR + ((SH || X2 || (HAFB_SHFL_PIVOT && S >= 26 && !HAFB_NS)) ? 0 : 2 * SP);
-    static constexpr int CF = MU + (X2 ? 4 * S : 2 * SP);  // [2][S] charpoly coefs
+    // [2][SP] multipliers (the window variant for S >= 26 shuffles the pivot row: no PR)
+    static constexpr int MU = PR + ((SH || (HAFB_SHFL_PIVOT && S >= 26 && !HAFB_NS)) ? 0 : 2 * SP);
+    static constexpr int CF = MU + 2 * SP;            // [2][S] charpoly coefs
     static constexpr int RED = CF + 2 * S;            // [2][2][2] argmax exchange (W = 64)
     static constexpr int A = RED + 8;                 // [S+1] charpoly coefficients
     static constexpr int U = A + S + 1;               // [2][S] loop-chain vector (LOOPS)
@@ -595,7 +598,7 @@ __device__ __forceinline__ void ns_read(const cd (&w)[S], int b, cd& v) {
 
 template <int S, int W>
 __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const TeamCtx<W>& tc, cd* ws) {
-    static_assert(W == 32, "NS variant: one warp per subset");
+    static_assert(W == 32 || W == 64, "NS variant: one or two warps per subset");
     using L = FastLayout<S>;
     cd* Hs = ws + L::HS;
     cd* pr = ws + L::PR;  // pivot row, by logical column
@@ -617,8 +620,32 @@ __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const Team
 #else
         const unsigned kb = key > 0.0 ? __float_as_uint(__double2float_ru(key)) : 0u;
 #endif
-        const unsigned mx = __reduce_max_sync(0xffffffffu, (kb & ~63u) | (unsigned)(63 - lane));
-        const int wl = 63 - (int)(mx & 63u);
+        unsigned mx = __reduce_max_sync(0xffffffffu, (kb & ~63u) | (unsigned)(63 - lane));
+        int wl = 63 - (int)(mx & 63u);
+#if NS_SPECINV
+        cd ip;
+#endif
+        int brow;
+        if constexpr (W == 64) {
+            // each warp's winner posts (packed key, logical row, reciprocal); one barrier
+            const int src = wl & 31;
+            const int wrow = __shfl_sync(0xffffffffu, myrow, src);
+            cd winv;
+            winv.re = __shfl_sync(0xffffffffu, myinv.re, src);
+            winv.im = __shfl_sync(0xffffffffu, myinv.im, src);
+            cd* R = ws + L::RED + (J & 1) * 4;
+            if ((lane & 31) == 0) {
+                R[2 * (lane >> 5)] = mk((double)mx, (double)wrow);
+                R[2 * (lane >> 5) + 1] = winv;
+            }
+            tc.sync();
+            const cd a0 = R[0], a1 = R[2];
+            const bool second = a1.re > a0.re;
+            mx = (unsigned)(second ? a1.re : a0.re);
+            wl = 63 - (int)(mx & 63u);
+            brow = (int)(second ? a1.im : a0.im);
+            ip = second ? R[3] : R[1];
+        }
         const int CS = (J * (J + 3)) / 2;  // column J in the packed store
         if ((mx & ~63u) == 0u) {  // nothing to eliminate below the subdiagonal: no update
             if (myrow <= J + 1) Hs[CS + myrow] = hj;
@@ -626,12 +653,15 @@ __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const Team
             ns_read<S, 2, S>(w, J + 2, hn);
             continue;
         }
-        const int brow = __shfl_sync(0xffffffffu, myrow, wl);
 #if NS_SPECINV
-        cd ip;
-        ip.re = __shfl_sync(0xffffffffu, myinv.re, wl);
-        ip.im = __shfl_sync(0xffffffffu, myinv.im, wl);
+        if constexpr (W == 32) {
+            brow = __shfl_sync(0xffffffffu, myrow, wl);
+            ip.re = __shfl_sync(0xffffffffu, myinv.re, wl);
+            ip.im = __shfl_sync(0xffffffffu, myinv.im, wl);
+        }
 #else
+        static_assert(W == 32, "the two-warp NS variant needs NS_SPECINV");
+        brow = __shfl_sync(0xffffffffu, myrow, wl);
         cd p;
         p.re = __shfl_sync(0xffffffffu, hj.re, wl);
         p.im = __shfl_sync(0xffffffffu, hj.im, wl);
@@ -647,7 +677,9 @@ __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const Team
         if (brow != J + 1) ns_xchg<S, 2, S>(w, brow, hn);
         // publish the pivot row (logical row J+1): predicated stores, no per-column branch
         const bool pl = lane == wl;
-#if NS_PUBPRED
+#if NS_SHFLROW
+        (void)pl;
+#elif NS_PUBPRED
         if (pl) pr[J + 1] = hn;
         static_for<2, S>([&](auto cc) {
             constexpr int c = decltype(cc)::value;
@@ -657,18 +689,73 @@ __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const Team
 #else
         if (pl) {
             pr[J + 1] = hn;
-            static_for<0, S - 2>([&](auto ii) {
+            static_for<0, S - 2, 2>([&](auto ii) {
                 constexpr int c = S - 1 - decltype(ii)::value;
-                if (c < J + 2) return false;
                 pr[c] = w[c];
+                if (c - 1 >= J + 2) pr[c - 1] = w[c - 1];
+                if (c - 1 <= J + 2) return false;
                 return true;
             });
         }
 #endif
-        __syncwarp();
+        tc.sync();
         // sweep, columns S-1 down to J+2: row update fused with the column gemv; at J+2
         // stash the next step's column J+2 and finish column J+1 (the gemv target)
         cd acc0 = mk(0.0, 0.0), acc1 = mk(0.0, 0.0);
+#if NS_SHFLROW
+        // pivot-row entries by register shuffle from the pivot lane (its row is not updated)
+        auto pbc = [&](const cd& v) -> cd {
+            cd r;
+            r.re = __shfl_sync(0xffffffffu, v.re, wl);
+            r.im = __shfl_sync(0xffffffffu, v.im, wl);
+            return r;
+        };
+        const cd p1 = pbc(hn);
+        cd pa = pbc(w[S - 1]), ma = mus[S - 1];
+        static_for<0, S - 2>([&](auto ii) {
+            constexpr int c = S - 1 - decltype(ii)::value;
+            const cd pn = c - 1 >= 2 ? pbc(w[c - 1 >= 2 ? c - 1 : 2]) : p1;
+            const cd mn = mus[c - 1];
+            w[c] = f_cms(w[c], mu, pa);
+            if constexpr (c & 1) acc1 = f_cma(acc1, ma, w[c]);
+            else acc0 = f_cma(acc0, ma, w[c]);
+            pa = pn;
+            ma = mn;
+            if (c == J + 2) {
+                const cd nh = w[c];
+                hj = f_add(f_cms(hn, mu, p1), f_add(acc0, acc1));
+                hn = nh;
+                return false;
+            }
+            return true;
+        });
+#elif NS_PAIR
+        // columns in pairs (c, c-1) under one exit test: the pair that holds J+2 may also
+        // hold J+1, whose register copy is dead (it travels in hn) and whose multiplier is
+        // zero, so updating it is harmless
+        cd pa = pr[S - 1], ma = mus[S - 1], pb = pr[S - 2], mb = mus[S - 2];
+        static_for<0, S - 2, 2>([&](auto ii) {
+            constexpr int c = S - 1 - decltype(ii)::value;
+            const cd pn = pr[c - 2], mn = mus[c - 2];  // next pair's broadcasts
+            const cd pm = pr[c >= 3 ? c - 3 : 0], mm = mus[c >= 3 ? c - 3 : 0];
+            w[c] = f_cms(w[c], mu, pa);
+            w[c - 1] = f_cms(w[c - 1], mu, pb);
+            acc1 = f_cma(acc1, ma, w[c]);
+            acc0 = f_cma(acc0, mb, w[c - 1]);
+            if (c - 1 <= J + 2) {
+                const cd nh = c == J + 2 ? w[c] : w[c - 1];
+                const cd p1 = pr[J + 1];
+                hj = f_add(f_cms(hn, mu, p1), f_add(acc0, acc1));
+                hn = nh;
+                return false;
+            }
+            pa = pn;
+            ma = mn;
+            pb = pm;
+            mb = mm;
+            return true;
+        });
+#else
         cd pa = pr[S - 1], ma = mus[S - 1];
         static_for<0, S - 2>([&](auto ii) {
             constexpr int c = S - 1 - decltype(ii)::value;
@@ -686,259 +773,13 @@ __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const Team
             }
             return true;
         });
+#endif
     }
     // logical columns S-2 (hj) and S-1 (hn): every row
     if (myrow < S) {
         Hs[((S - 2) * (S + 1)) / 2 + myrow] = hj;
         Hs[((S - 1) * (S + 2)) / 2 + myrow] = hn;
     }
-}
-
-// ============================================================================ X2 layout
-// Hessenberg reduction with each lane holding TWO rows and HALF of the columns
-// (column-cyclic): lane = 2g + h owns physical rows 2g, 2g+1 (slots 0, 1) and the
-// columns c = 2k + h.  Every broadcast operand of the sweep (the pivot-row entry of
-// column c and the multiplier of logical row c) then feeds 16 DFMA (two rows) instead
-// of 8, which halves the shared-memory / shuffle traffic per DFMA -- on B200 a
-// warp-wide broadcast LDS.128 issues at ~0.5/clk/SM and SHFL at ~1/clk/SM against
-// ~1.8 warp-DFMA/clk/SM (tools/micro/shfl.cu), so the one-row-per-lane sweep was
-// bound by its broadcasts.  The two halves of a row meet in one shfl.xor per step
-// (the column gemv's partial sums).  Same arithmetic identities as fast_hessenberg;
-// window positions k of a half hold columns 2(k0 + k) + h after k0 = J0/2 shifts.
-template <int S>
-__device__ __forceinline__ cd x2_shfl_xor1(cd v) {
-    cd r;
-    r.re = __shfl_xor_sync(0xffffffffu, v.re, 1);
-    r.im = __shfl_xor_sync(0xffffffffu, v.im, 1);
-    return r;
-}
-
-// v_s = w[s][pb] / w[s][pb] = v_s (if en) for a team-uniform runtime pb in [LO, HI)
-template <int S, int LO, int HI>
-__device__ __forceinline__ void x2_read(const cd (&w)[2][S / 2], int pb, cd& v0, cd& v1) {
-    if constexpr (HI - LO == 1) {
-        v0 = w[0][LO];
-        v1 = w[1][LO];
-    } else if constexpr (HI > LO) {
-        constexpr int MID = (LO + HI) / 2;
-        if (pb < MID) x2_read<S, LO, MID>(w, pb, v0, v1);
-        else x2_read<S, MID, HI>(w, pb, v0, v1);
-    }
-}
-template <int S, int LO, int HI>
-__device__ __forceinline__ void x2_write(cd (&w)[2][S / 2], int pb, bool en, const cd& v0, const cd& v1) {
-    if constexpr (HI - LO == 1) {
-        if (en) {
-            w[0][LO] = v0;
-            w[1][LO] = v1;
-        }
-    } else if constexpr (HI > LO) {
-        constexpr int MID = (LO + HI) / 2;
-        if (pb < MID) x2_write<S, LO, MID>(w, pb, en, v0, v1);
-        else x2_write<S, MID, HI>(w, pb, en, v0, v1);
-    }
-}
-
-// swap logical columns J+1 (half HA, window position PA) and brow (half b, position pb)
-template <int S, int HA, int PA>
-__device__ __forceinline__ void x2_colswap(cd (&w)[2][S / 2], int pb, bool same, int h) {
-    constexpr int KW = S / 2;
-    const bool ha = h == HA;
-    cd v0, v1;
-    x2_read<S, PA, KW>(w, pb, v0, v1);
-    const cd a0 = w[0][PA], a1 = w[1][PA];
-    cd n0, n1;  // new values of position pb
-    if (same) {
-        n0 = a0;
-        n1 = a1;
-    } else {
-        // the partner lane (other half, same rows) holds the other column
-        const cd o0 = ha ? a0 : v0, o1 = ha ? a1 : v1;
-        n0 = x2_shfl_xor1<S>(o0);
-        n1 = x2_shfl_xor1<S>(o1);
-        v0 = n0;
-        v1 = n1;
-    }
-    // half HA: position PA <- column brow (own if same, else the partner's);
-    // position pb <- column J+1: own (same, half HA) or the partner's (!same, half b)
-    if (ha) {
-        w[0][PA] = v0;
-        w[1][PA] = v1;
-    }
-    x2_write<S, PA, KW>(w, pb, same ? ha : !ha, n0, n1);
-}
-
-// One step J = J0 + OFF (OFF = 0..3) of the reduction on the X2 window: at the group
-// start J0 (a multiple of 2), position k of half h holds logical column 2(k0 + k) + h.
-template <int S, int OFF, bool LOOPS>
-__device__ __forceinline__ void x2_step(cd (&w)[2][S / 2], int (&lr)[2], const int J0,
-                                        const TeamCtx<32>& tc, cd* ws) {
-    using L = FastLayout<S, false, LOOPS, true>;
-    constexpr int KW = S / 2;
-    constexpr int HJ = OFF & 1, PJ = OFF >> 1;              // column J: half, position
-    constexpr int HA = (OFF + 1) & 1, PA = (OFF + 1) >> 1;  // column J+1
-    const int J = J0 + OFF;
-    const int k0 = J0 >> 1;
-    const int live = KW - k0;  // live window positions per half
-    const int lane = tc.lane, g = lane >> 1, h = lane & 1;
-    cd* Hs = ws + L::HS;
-    cd* X = ws + L::MU + (OFF & 1) * 2 * S;  // X[2c] = pivot-row entry, X[2c+1] = multiplier of row c
-    // ---- pivot search over column J; ties -> lowest physical row
-    unsigned pk = 0;
-    if (h == HJ) {
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-            const cd v = w[s][PJ];
-            const double key = (lr[s] > J && lr[s] < S) ? fabs(v.re) + fabs(v.im) : 0.0;
-            const unsigned kb = key > 0.0 ? __float_as_uint(__double2float_ru(key)) : 0u;
-            const unsigned pc = (kb & ~63u) | (unsigned)(63 - (2 * g + s));
-            pk = pc > pk ? pc : pk;
-        }
-    }
-    const unsigned mx = __reduce_max_sync(0xffffffffu, pk);
-    const int CS = (J * (J + 3)) / 2;  // column J in the packed store
-    if ((mx & ~63u) == 0u) {  // nothing to eliminate below the subdiagonal
-        if (h == HJ) {
-#pragma unroll
-            for (int s = 0; s < 2; ++s)
-                if (lr[s] <= J + 1) Hs[CS + lr[s]] = w[s][PJ];
-        }
-        return;
-    }
-    const int pw = 63 - (int)(mx & 63u);  // physical pivot row
-    const int ps = pw & 1;
-    const int src = (pw >> 1) * 2 + HJ;
-    const cd mine = ps ? w[1][PJ] : w[0][PJ];
-    const int mylab = ps ? lr[1] : lr[0];
-    cd p;
-    p.re = __shfl_sync(0xffffffffu, mine.re, src);
-    p.im = __shfl_sync(0xffffffffu, mine.im, src);
-    const int brow = __shfl_sync(0xffffffffu, mylab, src);
-    const cd ip = f_inv(p);
-    // ---- row swap J+1 <-> brow as a relabelling
-#pragma unroll
-    for (int s = 0; s < 2; ++s) lr[s] = lr[s] == brow ? J + 1 : (lr[s] == J + 1 ? brow : lr[s]);
-    if (h == HJ) {
-#pragma unroll
-        for (int s = 0; s < 2; ++s)
-            if (lr[s] <= J + 1) Hs[CS + lr[s]] = w[s][PJ];
-    }
-    // ---- column swap J+1 <-> brow
-    if (brow != J + 1) {
-        const int b = brow & 1;
-        const int pb = ((brow - b) >> 1) - k0;
-        x2_colswap<S, HA, PA>(w, pb, b == HA, h);
-    }
-    // ---- multipliers (half HJ holds column J) and the pivot row, published per logical column
-    cd mu[2];
-    if (h == HJ) {
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-            const bool elim = lr[s] >= J + 2 && lr[s] < S;
-            mu[s] = elim ? f_mul(w[s][PJ], ip) : mk(0.0, 0.0);
-            if (lr[s] < S) X[2 * lr[s] + 1] = mu[s];
-        }
-    }
-    {
-        // the two lanes holding the pivot row store its entries; the slot choice is
-        // warp-uniform, the lane predicate is applied per store (no divergent branch)
-        const bool pl = g == (pw >> 1);
-        cd* Xp = X + 2 * (2 * k0 + h);
-        if (ps) {
-            static_for<PJ, KW>([&](auto kk) {
-                constexpr int k = decltype(kk)::value;
-                if (k < live) {
-                    if (pl) Xp[4 * k] = w[1][k];
-                }
-                return true;
-            });
-        } else {
-            static_for<PJ, KW>([&](auto kk) {
-                constexpr int k = decltype(kk)::value;
-                if (k < live) {
-                    if (pl) Xp[4 * k] = w[0][k];
-                }
-                return true;
-            });
-        }
-    }
-    __syncwarp();
-    if (h != HJ) {
-#pragma unroll
-        for (int s = 0; s < 2; ++s) mu[s] = lr[s] < S ? X[2 * lr[s] + 1] : mk(0.0, 0.0);
-    }
-    // ---- sweep: rank-1 row update fused with the column gemv.  Positions from PJ on
-    //      cover every column >= J+1; the few columns <= J it also touches are final
-    //      (stored) and have zero multipliers, so they add nothing to the gemv.
-    cd acc0 = mk(0.0, 0.0), acc1 = mk(0.0, 0.0);
-    const cd* Xh = X + 2 * (2 * k0 + h);
-    static_for<PJ, KW>([&](auto kk) {
-        constexpr int k = decltype(kk)::value;
-        if (k < live) {
-            const cd pc = Xh[4 * k], mc = Xh[4 * k + 1];
-            w[0][k] = f_cms(w[0][k], mu[0], pc);
-            w[1][k] = f_cms(w[1][k], mu[1], pc);
-            acc0 = f_cma(acc0, mc, w[0][k]);
-            acc1 = f_cma(acc1, mc, w[1][k]);
-        }
-        return true;
-    });
-    const cd t0 = x2_shfl_xor1<S>(acc0), t1 = x2_shfl_xor1<S>(acc1);
-    if (h == HA) {  // column J+1
-        w[0][PA] = f_add(w[0][PA], f_add(acc0, t0));
-        w[1][PA] = f_add(w[1][PA], f_add(acc1, t1));
-    }
-}
-
-#ifndef HAFB_X2_GROUP
-#define HAFB_X2_GROUP 4
-#endif
-
-template <int S, int NSH>
-__device__ __forceinline__ void x2_shift(cd (&w)[2][S / 2]) {
-    // shift the window by NSH columns per half (dead positions shift too: plain moves)
-    static_for<0, S / 2 - NSH>([&](auto kk) {
-        constexpr int k = decltype(kk)::value;
-        w[0][k] = w[0][k + NSH];
-        w[1][k] = w[1][k + NSH];
-        return true;
-    });
-}
-
-template <int S, bool LOOPS>
-__device__ __forceinline__ void x2_hessenberg(cd (&w)[2][S / 2], int (&lr)[2], const TeamCtx<32>& tc,
-                                              cd* ws) {
-    using L = FastLayout<S, false, LOOPS, true>;
-    int J0 = 0;
-    if constexpr (HAFB_X2_GROUP == 4) {
-        // groups of four steps per window shift of two (half the register moves)
-#pragma unroll 1
-        for (; J0 + 4 <= S - 2; J0 += 4) {
-            x2_step<S, 0, LOOPS>(w, lr, J0, tc, ws);
-            x2_step<S, 1, LOOPS>(w, lr, J0, tc, ws);
-            x2_step<S, 2, LOOPS>(w, lr, J0, tc, ws);
-            x2_step<S, 3, LOOPS>(w, lr, J0, tc, ws);
-            x2_shift<S, 2>(w);
-        }
-        if (J0 < S - 2) {  // S - 2 = 2 (mod 4): one pair left
-            x2_step<S, 0, LOOPS>(w, lr, J0, tc, ws);
-            x2_step<S, 1, LOOPS>(w, lr, J0, tc, ws);
-            x2_shift<S, 1>(w);
-        }
-    } else {
-#pragma unroll 1
-        for (; J0 < S - 2; J0 += 2) {
-            x2_step<S, 0, LOOPS>(w, lr, J0, tc, ws);
-            x2_step<S, 1, LOOPS>(w, lr, J0, tc, ws);
-            x2_shift<S, 1>(w);
-        }
-    }
-    // logical columns S-2 (half 0) and S-1 (half 1) are at window position 0
-    cd* Hs = ws + L::HS;
-    const int c = S - 2 + (tc.lane & 1);
-#pragma unroll
-    for (int s = 0; s < 2; ++s)
-        if (lr[s] < S) Hs[(c * (c + 3)) / 2 + lr[s]] = w[s][0];
 }
 
 template <int S, bool LOOPS, bool SH, int NT = kFastThreads>
@@ -955,8 +796,7 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
     // blocks of more than 128 threads (one block per SM) keep their teams in the same
     // phase so the SM's instruction cache holds one phase's code at a time
     constexpr bool PSYNC = NT > kFastThreads;
-    constexpr bool X2 = !SH && x2_variant(S);
-    using L = FastLayout<S, SH, LOOPS, X2>;
+    using L = FastLayout<S, SH, LOOPS>;
     extern __shared__ cd smem[];
     TeamCtx<W> tc;
     tc.tib = threadIdx.x / W;
@@ -1086,24 +926,6 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
             tc.sync();
             HT_MARK(0);
             smem_hessenberg<S, W, LOOPS>(H, myrow, tc, ws);
-        } else if constexpr (X2) {
-            // lane 2g+h: rows 2g, 2g+1 (vertices 2 v_g, 2 v_g + 1), columns 2k+h (vertex 2 v_k + h)
-            constexpr int KW = S / 2;
-            const int g = lane >> 1, h = lane & 1;
-            const int gb = g < M ? (int)__fns(ir.mask, 0, g + 1) : 0;
-            cd w2[2][KW];
-            int lr[2] = {2 * g, 2 * g + 1};
-            gather([&](const cd* src, int ld) {
-                static_for<0, KW>([&](auto kk) {
-                    constexpr int k = decltype(kk)::value;
-                    const int vc = 2 * vbit[k] + h;
-                    w2[0][k] = g < M ? src[(2 * gb) * ld + vc] : mk(0.0, 0.0);
-                    w2[1][k] = g < M ? src[(2 * gb + 1) * ld + vc] : mk(0.0, 0.0);
-                    return true;
-                });
-            });
-            HT_MARK(0);
-            x2_hessenberg<S, LOOPS>(w2, lr, tc, ws);
         } else {
             gather([&](const cd* src, int ld) {
                 static_for<0, S>([&](auto c) {
@@ -1139,6 +961,57 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
             cd P[S];
             P[0] = mk(lane == 0 ? 1.0 : 0.0, 0.0);
             cd prodl = mk(1.0, 0.0);
+            if constexpr (!SH && W <= 32 && HAFB_CPRE) {
+                // The recurrence's coefficients cf(k, l) = h(l, k-1) prod_{j=l+1}^{k-1} h(j, j-1)
+                // do not depend on the polynomials: lane l forms them all up front (its running
+                // subdiagonal product, same operation order as the per-step form below) and
+                // stores them IN PLACE over h(l, k-1) -- the diagonal and the subdiagonal the
+                // recurrence still reads are never overwritten.  The recurrence then runs
+                // without a barrier per step and the compiler overlaps consecutive steps.
+                cd* Hm = ws + L::HS;
+                cd prod = mk(1.0, 0.0);
+                // branch-free: every lane runs every column (lanes >= c compute and drop)
+                const int lsafe = lane < S ? lane : 0;
+                static_for<1, S>([&](auto cc) {
+                    constexpr int c = decltype(cc)::value;
+                    const cd beta = Hm[((c - 1) * (c + 2)) / 2 + c];  // h[c][c-1]
+                    const cd np = f_mul(lane == c - 1 ? mk(1.0, 0.0) : prod, beta);
+                    const bool on = lane < c;
+                    prod = on ? np : prod;
+                    cd* e = Hm + (c * (c + 3)) / 2 + (on ? lane : lsafe);
+                    const cd v = f_mul(*e, prod);
+                    if (on) *e = v;
+                    return true;
+                });
+                tc.sync();
+                static_for<1, S + 1>([&](auto kk) {
+                    constexpr int k = decltype(kk)::value;
+                    const cd* cfk = Hm + ((k - 1) * (k + 2)) / 2;  // cf(k, l) at l, h(k-1,k-1) at k-1
+                    cd prev;
+                    prev.re = tshfl_up<W>(P[k - 1].re, 1);
+                    prev.im = tshfl_up<W>(P[k - 1].im, 1);
+                    if (lane == 0) prev = mk(0.0, 0.0);
+                    cd acc = f_cms(prev, cfk[k - 1], P[k - 1]);
+                    cd acc2 = mk(0.0, 0.0), acc3 = mk(0.0, 0.0), acc4 = mk(0.0, 0.0);
+                    static_for<1, k, 4>([&](auto ii) {
+                        constexpr int i0 = decltype(ii)::value;
+                        if (i0 >= k + opaque_zero) return false;
+                        static_for<i0, (i0 + 4 < k ? i0 + 4 : k)>([&](auto jj) {
+                            constexpr int i = decltype(jj)::value;
+                            if constexpr ((i & 3) == 0) acc = f_cms(acc, cfk[i - 1], P[i - 1]);
+                            else if constexpr ((i & 3) == 1) acc2 = f_cms(acc2, cfk[i - 1], P[i - 1]);
+                            else if constexpr ((i & 3) == 2) acc3 = f_cms(acc3, cfk[i - 1], P[i - 1]);
+                            else acc4 = f_cms(acc4, cfk[i - 1], P[i - 1]);
+                            return true;
+                        });
+                        return true;
+                    });
+                    acc = f_add(f_add(acc, acc2), f_add(acc3, acc4));
+                    if constexpr (k < S) P[k] = acc;
+                    else if (lane < S) A[lane] = acc;
+                    return true;
+                });
+            } else
             static_for<1, S + 1>([&](auto kk) {
                 constexpr int k = decltype(kk)::value;
                 cd* cf = ws + L::CF + (k & 1) * S;

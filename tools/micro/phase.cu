@@ -41,7 +41,7 @@ int main(int argc, char** argv) {
 #define SHV true
 #endif
     const int stage = (NTV > kFastThreads && !SHV) ? 1 : 0;
-    size_t smem = (size_t)TPB * FastLayout<HAFB_S, SHV, false, !SHV && x2_variant(HAFB_S)>::TOTAL * sizeof(cd) + (kDMax + 1) * 8 + (stage ? (size_t)n * (n + 1) * sizeof(cd) : 0);
+    size_t smem = (size_t)TPB * FastLayout<HAFB_S, SHV, false>::TOTAL * sizeof(cd) + (kDMax + 1) * 8 + (stage ? (size_t)n * (n + 1) * sizeof(cd) : 0);
     auto k = fast_term_kernel<HAFB_S, false, SHV, NTV>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int occ; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NTV, smem);

@@ -94,6 +94,9 @@ constexpr int kDMax = 31;
 #ifndef NS_PAIR
 #define NS_PAIR 0
 #endif
+#ifndef HAFB_QSERIES
+#define HAFB_QSERIES 1
+#endif
 #ifndef HAFB_CPRE
 #define HAFB_CPRE 0
 #endif
@@ -1066,6 +1069,43 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
         cd* T = ws + L::T;
         cd* A = ws + L::A;
         int bad = 0;
+        cd eD = mk(0.0, 0.0);
+        constexpr bool QS = !LOOPS && W == 32 && HAFB_QSERIES;
+        if constexpr (QS) {
+            // Without loop weights the series is exp(sum_k t_k x^k / (2k)) = q(x)^(-1/2) with
+            // q(x) = det(I - xB) = sum_j a_j x^j, a_j = A[S-j] (the reversed charpoly), so
+            // Newton's identities and the exp recurrence (_numba.py:228-250, :276-294)
+            // collapse into ONE recurrence from q g' = -(1/2) q' g:
+            //   g_0 = 1,  g_k = -(1/k) sum_{j=1}^{min(k,S)} a_j (k - j/2) g_{k-j},
+            // evaluated in push form (lane k-1 accumulates g_k; each g_m is broadcast once).
+            // Exact in exact arithmetic; a non-finite coefficient or result -> status 2.
+            static_assert(R == 1, "one coefficient chunk per lane");
+            const int k = lane + 1;
+            cd acc = mk(0.0, 0.0);
+            const int src0 = ((int)(threadIdx.x & 31) & ~(W - 1));
+            for (int m = 0; m < D; ++m) {
+                cd gm;
+                if (m == 0) {
+                    gm = mk(1.0, 0.0);
+                } else {
+                    const double sc = -INV[m];
+                    gm.re = __shfl_sync(tc.wmask, acc.re, src0 + m - 1) * sc;
+                    gm.im = __shfl_sync(tc.wmask, acc.im, src0 + m - 1) * sc;
+                }
+                const int j = k - m;
+                if (k <= D && j >= 1 && j <= S) {
+                    const double wgt = 0.5 * (double)(k + m);
+                    acc = f_cma(acc, A[S - j], mk(wgt * gm.re, wgt * gm.im));
+                }
+            }
+            if (lane < S + 1) {
+                const cd a = A[lane];
+                if (!isfinite(a.re) || !isfinite(a.im)) bad = 1;
+            }
+            eD = mk(-acc.re * INV[D], -acc.im * INV[D]);
+            if (lane == D - 1 && (!isfinite(eD.re) || !isfinite(eD.im))) bad = 1;
+            bad = __any_sync(tc.wmask, bad);
+        } else {
         {
             cd acck[R];
 #pragma unroll
@@ -1125,7 +1165,7 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
         }
         tc.sync();
         // ---------------------------------------------- exp coefficient: e_k = (1/k) sum_j g_j e_{k-j}
-        cd eD = mk(0.0, 0.0);
+        eD = mk(0.0, 0.0);
         {
             cd acck[R];
 #pragma unroll
@@ -1172,6 +1212,7 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
                 for (int r = 0; r < R; ++r)
                     if (r == chunk) eD = mk(acck[r].re * INV[D], acck[r].im * INV[D]);
             }
+        }
         }
         if (valid && lane == ((D - 1) % W)) {
             const bool neg = ((D - M) & 1) != 0;

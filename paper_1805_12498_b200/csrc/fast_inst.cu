@@ -43,13 +43,19 @@ constexpr int threads_for(int S) {
            : kFastThreads;
 }
 
+#ifndef HAFB_NSX_THREADS
+#define HAFB_NSX_THREADS 256
+#endif
+
 template <int S, bool L>
 static cudaError_t launch_one(const cd* at, const cd* dg, int n_half, const ClassItems& ci,
                               cd* terms, int8_t* status, cudaStream_t st, int sms) {
-    constexpr int W = TeamWidth<S>::W;
-    constexpr int NT = threads_for(S);
+    // S = 34, 36 without loops: one-warp teams with the extra rows held column-wise
+    constexpr bool NSX = nsx_variant(S) && !L;
+    constexpr bool SH = smem_hess(S) && !NSX;
+    constexpr int W = FastTeam<S, L, SH>::W;
+    constexpr int NT = NSX ? HAFB_NSX_THREADS : threads_for(S);
     constexpr int TPB = NT / W;
-    constexpr bool SH = smem_hess(S);
     const size_t base_smem = (size_t)TPB * FastLayout<S, SH, L>::TOTAL * sizeof(cd) + (kDMax + 1) * sizeof(double);
     // the one-block-per-SM register classes stage Atilde in shared memory when it fits
     const int n = 2 * n_half;

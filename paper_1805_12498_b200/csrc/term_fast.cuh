@@ -785,6 +785,232 @@ __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const Team
     }
 }
 
+
+// ============================================================================ NSX variant
+// S = 32 + E (E = 2, 4): one warp per subset.  Rows 0..31 are lane rows exactly as in
+// ns_hessenberg; the E extra rows are held COLUMN-wise: lane l keeps their entries of
+// columns l (slot 0) and 32 + l (slot 1, lanes < E), so no second warp idles on E rows.
+// Per step the extra rows cost: their pivot candidates (lane J & 31), a shuffle pair for
+// the column swap, an E-row rank-1 update + gemv partial per lane, and one butterfly
+// all-reduce of the E gemv partials.  Same arithmetic identities as ns_hessenberg.
+#ifndef HAFB_NSX
+#define HAFB_NSX 1
+#endif
+constexpr bool nsx_variant(int S) { return HAFB_NSX && (S == 34 || S == 36); }
+
+template <int E>
+__device__ __forceinline__ cd nsx_slot(const cd (&x)[2], bool hi) { return hi ? x[1] : x[0]; }
+
+template <int S>
+__device__ __forceinline__ void nsx_hessenberg(cd (&w)[S], cd (&ex)[S - 32][2], int& myrow,
+                                               int (&elab)[S - 32], const TeamCtx<32>& tc, cd* ws) {
+    constexpr int E = S - 32;
+    using L = FastLayout<S>;
+    cd* Hs = ws + L::HS;
+    cd* pr = ws + L::PR;
+    cd* mus = ws + L::MU;
+    const int lane = tc.lane;
+    cd hj = w[0], hn = w[1];
+#pragma unroll 1
+    for (int J = 0; J < S - 2; ++J) {
+        const int jl = J & 31;
+        const bool js = J >= 32;
+        cd xv[E];  // extra rows' column-J entries (meaningful in lane jl)
+#pragma unroll
+        for (int e = 0; e < E; ++e) xv[e] = js ? ex[e][1] : ex[e][0];
+        const double key = (myrow > J && myrow < S) ? fabs(hj.re) + fabs(hj.im) : 0.0;
+        const cd myinv = f_inv(hj);
+        unsigned pk = ((unsigned)__double2hiint(key) & ~63u) | (unsigned)(63 - lane);
+        if (lane == jl) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const double kx = elab[e] > J ? fabs(xv[e].re) + fabs(xv[e].im) : 0.0;
+                const unsigned c = ((unsigned)__double2hiint(kx) & ~63u) | (unsigned)(63 - (32 + e));
+                pk = c > pk ? c : pk;
+            }
+        }
+        const unsigned mx = __reduce_max_sync(0xffffffffu, pk);
+        const int pw = 63 - (int)(mx & 63u);  // physical pivot row (>= 32: an extra row)
+        const int CS = (J * (J + 3)) / 2;
+        if ((mx & ~63u) == 0u) {  // nothing to eliminate below the subdiagonal
+            if (myrow <= J + 1) Hs[CS + myrow] = hj;
+            if (lane == jl) {
+#pragma unroll
+                for (int e = 0; e < E; ++e)
+                    if (elab[e] <= J + 1) Hs[CS + elab[e]] = xv[e];
+            }
+            hj = hn;
+            ns_read<S, 2, S>(w, J + 2, hn);
+            continue;
+        }
+        int brow;
+        cd ip;
+        if (pw < 32) {
+            brow = __shfl_sync(0xffffffffu, myrow, pw);
+            ip.re = __shfl_sync(0xffffffffu, myinv.re, pw);
+            ip.im = __shfl_sync(0xffffffffu, myinv.im, pw);
+        } else {
+            cd v = xv[0];
+            int lb = elab[0];
+#pragma unroll
+            for (int e = 1; e < E; ++e)
+                if (pw - 32 == e) {
+                    v = xv[e];
+                    lb = elab[e];
+                }
+            cd p;
+            p.re = __shfl_sync(0xffffffffu, v.re, jl);
+            p.im = __shfl_sync(0xffffffffu, v.im, jl);
+            ip = f_inv(p);
+            brow = lb;
+        }
+        if (myrow == brow) myrow = J + 1;
+        else if (myrow == J + 1) myrow = brow;
+#pragma unroll
+        for (int e = 0; e < E; ++e) elab[e] = elab[e] == brow ? J + 1 : (elab[e] == J + 1 ? brow : elab[e]);
+        // multipliers of every logical row (all S rewritten each step) and column J's store
+        const bool elim = myrow >= J + 2 && myrow < S;
+        const cd mu = elim ? f_mul(hj, ip) : mk(0.0, 0.0);
+        mus[myrow] = mu;
+        if (myrow <= J + 1) Hs[CS + myrow] = hj;
+        if (lane == jl) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                mus[elab[e]] = elab[e] >= J + 2 ? f_mul(xv[e], ip) : mk(0.0, 0.0);
+                if (elab[e] <= J + 1) Hs[CS + elab[e]] = xv[e];
+            }
+        }
+        // column swap J+1 <-> brow: lane rows by the register tree; extra rows by lanes
+        if (brow != J + 1) {
+            ns_xchg<S, 2, S>(w, brow, hn);
+            const int a = (J + 1) & 31, b = brow & 31;
+            const bool sa = J + 1 >= 32, sb = brow >= 32;
+            if (a == b) {  // same lane, the two slots
+                if (lane == a) {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        const cd t = ex[e][0];
+                        ex[e][0] = ex[e][1];
+                        ex[e][1] = t;
+                    }
+                }
+            } else {
+                const int src = lane == a ? b : a;
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const cd out = lane == a ? (sa ? ex[e][1] : ex[e][0]) : (sb ? ex[e][1] : ex[e][0]);
+                    cd in;
+                    in.re = __shfl_sync(0xffffffffu, out.re, src);
+                    in.im = __shfl_sync(0xffffffffu, out.im, src);
+                    if (lane == a) {
+                        if (sa) ex[e][1] = in;
+                        else ex[e][0] = in;
+                    }
+                    if (lane == b) {
+                        if (sb) ex[e][1] = in;
+                        else ex[e][0] = in;
+                    }
+                }
+            }
+        }
+        // publish the pivot row (logical row J+1) by logical column
+        if (pw < 32) {
+            if (lane == pw) {
+                pr[J + 1] = hn;
+                static_for<0, S - 2>([&](auto ii) {
+                    constexpr int c = S - 1 - decltype(ii)::value;
+                    if (c < J + 2) return false;
+                    pr[c] = w[c];
+                    return true;
+                });
+            }
+        } else {
+            cd r0 = ex[0][0], r1 = ex[0][1];
+#pragma unroll
+            for (int e = 1; e < E; ++e)
+                if (pw - 32 == e) {
+                    r0 = ex[e][0];
+                    r1 = ex[e][1];
+                }
+            pr[lane] = r0;
+            if (lane < E) pr[32 + lane] = r1;
+        }
+        __syncwarp();
+        cd mue[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) mue[e] = mus[elab[e]];
+        // lane rows: sweep S-1 .. J+2 as in ns_hessenberg
+        cd acc0 = mk(0.0, 0.0), acc1 = mk(0.0, 0.0);
+        cd pa = pr[S - 1], ma = mus[S - 1];
+        static_for<0, S - 2>([&](auto ii) {
+            constexpr int c = S - 1 - decltype(ii)::value;
+            const cd pn = pr[c - 1], mn = mus[c - 1];
+            w[c] = f_cms(w[c], mu, pa);
+            if constexpr (c & 1) acc1 = f_cma(acc1, ma, w[c]);
+            else acc0 = f_cma(acc0, ma, w[c]);
+            pa = pn;
+            ma = mn;
+            if (c == J + 2) {
+                const cd nh = w[c];
+                hj = f_add(f_cms(hn, mu, pa), f_add(acc0, acc1));
+                hn = nh;
+                return false;
+            }
+            return true;
+        });
+        // extra rows: rank-1 update of my live columns (c >= J+1) and the gemv partials.
+        // Finished columns are left alone: the pivot-row buffer holds stale entries there,
+        // and a dead entry driven to inf would turn a zero multiplier's product into NaN.
+        cd part[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) part[e] = mk(0.0, 0.0);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int c = lane + 32 * q;
+            if ((q == 0 || lane < E) && c >= J + 1) {
+                const cd pc = pr[c], mc = mus[c];
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    ex[e][q] = f_cms(ex[e][q], mue[e], pc);
+                    part[e] = f_cma(part[e], mc, ex[e][q]);
+                }
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                part[e].re += __shfl_xor_sync(0xffffffffu, part[e].re, off);
+                part[e].im += __shfl_xor_sync(0xffffffffu, part[e].im, off);
+            }
+        }
+        // column J+1 of the extra rows (lane (J+1) & 31, its slot): += gemv
+        if (lane == ((J + 1) & 31)) {
+            const bool s1 = J + 1 >= 32;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                if (s1) ex[e][1] = f_add(ex[e][1], part[e]);
+                else ex[e][0] = f_add(ex[e][0], part[e]);
+            }
+        }
+    }
+    // logical columns S-2 and S-1: every row
+    Hs[((S - 2) * (S + 1)) / 2 + myrow] = hj;
+    Hs[((S - 1) * (S + 2)) / 2 + myrow] = hn;
+    if (lane == ((S - 2) & 31) || lane == ((S - 1) & 31)) {
+        const int c = 32 + lane;  // both are slot-1 columns (S - 2 >= 32)
+#pragma unroll
+        for (int e = 0; e < E; ++e) Hs[(c * (c + 3)) / 2 + elab[e]] = ex[e][1];
+    }
+}
+
+// team width of the FAST kernel: NSX sizes (no loops) run one-warp teams
+template <int S, bool LOOPS, bool SH>
+struct FastTeam {
+    static constexpr bool NSX = nsx_variant(S) && !LOOPS && !SH;
+    static constexpr int W = NSX ? 32 : TeamWidth<S>::W;
+};
+
 template <int S, bool LOOPS, bool SH, int NT = kFastThreads>
 __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ atilde,
                                                                  const cd* __restrict__ diag,
@@ -792,7 +1018,8 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
                                                                  cd* __restrict__ terms,
                                                                  int8_t* __restrict__ status,
                                                                  int stage_a) {
-    constexpr int W = TeamWidth<S>::W;
+    constexpr bool NSX = FastTeam<S, LOOPS, SH>::NSX;
+    constexpr int W = FastTeam<S, LOOPS, SH>::W;
     constexpr int TPB = NT / W;
     constexpr int M = S / 2;
     constexpr int R = (kDMax + W - 1) / W;  // coefficient chunks per lane
@@ -929,6 +1156,30 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
             tc.sync();
             HT_MARK(0);
             smem_hessenberg<S, W, LOOPS>(H, myrow, tc, ws);
+        } else if constexpr (NSX) {
+            constexpr int E = S - 32;
+            cd ex[E > 0 ? E : 1][2];
+            int elab[E > 0 ? E : 1];
+            // extra rows 32+e (vertices 2 v_{16+e/2} + (e&1), pair-swapped rows of Atilde),
+            // columns lane and 32+lane (vertices 2 v_{c/2} + (c&1))
+            const int cb1 = lane < E ? (int)__fns(ir.mask, 0, 16 + (lane >> 1) + 1) : 0;
+            gather([&](const cd* src, int ld) {
+                static_for<0, S>([&](auto c) {
+                    const int vc = 2 * vbit[c() >> 1] + (c() & 1);
+                    hr[c()] = src[vr * ld + vc];
+                    return true;
+                });
+                static_for<0, E>([&](auto ee) {
+                    constexpr int e = decltype(ee)::value;
+                    const int rv = 2 * vbit[16 + e / 2] + (e & 1);
+                    ex[e][0] = src[rv * ld + 2 * mybit + (lane & 1)];
+                    ex[e][1] = lane < E ? src[rv * ld + 2 * cb1 + (lane & 1)] : mk(0.0, 0.0);
+                    elab[e] = 32 + e;
+                    return true;
+                });
+            });
+            HT_MARK(0);
+            nsx_hessenberg<S>(hr, ex, myrow, elab, tc, ws);
         } else {
             gather([&](const cd* src, int ld) {
                 static_for<0, S>([&](auto c) {
@@ -964,6 +1215,8 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
             cd P[S];
             P[0] = mk(lane == 0 ? 1.0 : 0.0, 0.0);
             cd prodl = mk(1.0, 0.0);
+            cd prodx = mk(1.0, 0.0);
+            cd Q[NSX ? S - 32 : 1];  // extra coefficients (NSX)
             if constexpr (!SH && W <= 32 && HAFB_CPRE) {
                 // The recurrence's coefficients cf(k, l) = h(l, k-1) prod_{j=l+1}^{k-1} h(j, j-1)
                 // do not depend on the polynomials: lane l forms them all up front (its running
@@ -1024,6 +1277,12 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
                         prodl = f_mul(lane == k - 2 ? mk(1.0, 0.0) : prodl, beta);
                         cf[lane] = f_mul(hget_mine(k - 1), prodl);
                     }
+                    if constexpr (NSX && k >= 34) {  // rows 32 + lane of the extra coefficients
+                        if (lane < S - 32 && 32 + lane <= k - 2) {
+                            prodx = f_mul(32 + lane == k - 2 ? mk(1.0, 0.0) : prodx, beta);
+                            cf[32 + lane] = f_mul(hget(32 + lane, k - 1), prodx);
+                        }
+                    }
                 }
                 cd prev;
                 if constexpr (W <= 32) {
@@ -1056,6 +1315,30 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
                     return true;
                 });
                 acc = f_add(f_add(acc, acc2), f_add(acc3, acc4));
+                if constexpr (NSX && k >= 32) {
+                    // coefficients 32 + lane (lanes < E) of P_k: Q[t] = P_{32+t}[32+lane]
+                    constexpr int t = k - 32;
+                    cd pq;
+                    pq.re = __shfl_sync(0xffffffffu, P[k - 1].re, 31);
+                    pq.im = __shfl_sync(0xffffffffu, P[k - 1].im, 31);
+                    if constexpr (t >= 1) {
+                        cd up;
+                        up.re = __shfl_up_sync(0xffffffffu, Q[t - 1].re, 1);
+                        up.im = __shfl_up_sync(0xffffffffu, Q[t - 1].im, 1);
+                        if (lane != 0) pq = up;
+                    } else {
+                        if (lane != 0) pq = mk(0.0, 0.0);
+                    }
+                    cd q = pq;
+                    if constexpr (t >= 1) q = f_cms(q, hk, Q[t - 1]);
+                    static_for<32, k - 1>([&](auto ll) {
+                        constexpr int l = decltype(ll)::value;
+                        q = f_cms(q, cf[l], Q[l - 32]);
+                        return true;
+                    });
+                    if constexpr (k < S) Q[t] = q;
+                    else if (lane < S - 32) A[32 + lane] = q;
+                }
                 if constexpr (k < S) P[k] = acc;
                 else if (lane < S) A[lane] = acc;
                 return true;

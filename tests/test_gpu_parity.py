@@ -6,6 +6,8 @@ produced by the reference itself (tests/golden) and with the C oracle.
 FAST arithmetic is compared within the stated tolerances.
 """
 
+import itertools
+
 import numpy as np
 import pytest
 
@@ -370,3 +372,23 @@ def test_fast_terms_every_size_vs_oracle(S):
     scale = np.abs(ref).max()
     assert not st.any()
     assert np.abs(got - ref).max() <= 1e-10 * scale
+
+
+@pytest.mark.parametrize("S", [34, 36])
+def test_fast_extra_row_classes_full_class_vs_oracle(S):
+    """S = 34, 36 run one-warp teams with the rows beyond 32 held column-wise (NSX).
+    Every subset of the class for n = 44 (C(22, S/2) masks, thousands of teams walking
+    long mask runs): no failing status, every term within 1e-10 of the largest oracle
+    term, and a seeded sample checked per term against the bit-exact oracle."""
+    n = 44
+    A = random_symmetric(n, 2000 + S) / np.sqrt(n)
+    at, dg, nh = engine._prepare(A, False)
+    masks = np.array([sum(1 << b for b in c) for c in itertools.combinations(range(nh), S // 2)],
+                     dtype=np.uint64)
+    got, st = kernels.terms(at, dg, nh, masks, 1, False, arith="fast")
+    assert not st.any()
+    assert np.isfinite(got).all()
+    idx = np.random.default_rng(S).choice(masks.size, 1500, replace=False)
+    ref, _ = O.terms(at, dg, nh, masks[idx], backend=1)
+    scale = np.abs(ref).max()
+    assert np.abs(got[idx] - ref).max() <= 1e-10 * scale

@@ -36,7 +36,7 @@ int main(int argc, char** argv) {
     #ifndef NTV
 #define NTV kFastThreads
 #endif
-    constexpr int W = TeamWidth<HAFB_S>::W, TPB = NTV / W;
+    constexpr int W = FastTeam<HAFB_S, false, SHV>::W, TPB = NTV / W;
 #ifndef SHV
 #define SHV true
 #endif

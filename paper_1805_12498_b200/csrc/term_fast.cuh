@@ -94,6 +94,9 @@ constexpr int kDMax = 31;
 #ifndef NS_PAIR
 #define NS_PAIR 0
 #endif
+#ifndef HAFB_PSYNC
+#define HAFB_PSYNC 1
+#endif
 #ifndef HAFB_QSERIES
 #define HAFB_QSERIES 1
 #endif
@@ -1019,13 +1022,15 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
                                                                  int8_t* __restrict__ status,
                                                                  int stage_a) {
     constexpr bool NSX = FastTeam<S, LOOPS, SH>::NSX;
+    // blocks of more than 128 threads (one block per SM) keep their teams in the same phase
+    // (one phase's code in the instruction cache at a time) where that measured faster:
+    // the NSX classes (S = 34, 36: -15 %); the static-column classes S <= 32 run 2-3 %
+    // faster without the phase barriers
+    constexpr bool PSYNC = NT > kFastThreads && (NSX || (HAFB_PSYNC && !ns_variant(S)));
     constexpr int W = FastTeam<S, LOOPS, SH>::W;
     constexpr int TPB = NT / W;
     constexpr int M = S / 2;
     constexpr int R = (kDMax + W - 1) / W;  // coefficient chunks per lane
-    // blocks of more than 128 threads (one block per SM) keep their teams in the same
-    // phase so the SM's instruction cache holds one phase's code at a time
-    constexpr bool PSYNC = NT > kFastThreads;
     using L = FastLayout<S, SH, LOOPS>;
     extern __shared__ cd smem[];
     TeamCtx<W> tc;
@@ -1216,7 +1221,7 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
             P[0] = mk(lane == 0 ? 1.0 : 0.0, 0.0);
             cd prodl = mk(1.0, 0.0);
             cd prodx = mk(1.0, 0.0);
-            cd Q[NSX ? S - 32 : 1];  // extra coefficients (NSX)
+            cd Q[NSX ? S - 32 : 1] = {};  // extra coefficients (NSX)
             if constexpr (!SH && W <= 32 && HAFB_CPRE) {
                 // The recurrence's coefficients cf(k, l) = h(l, k-1) prod_{j=l+1}^{k-1} h(j, j-1)
                 // do not depend on the polynomials: lane l forms them all up front (its running

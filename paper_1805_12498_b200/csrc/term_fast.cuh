@@ -94,6 +94,11 @@ constexpr int kDMax = 31;
 #ifndef NS_PAIR
 #define NS_PAIR 0
 #endif
+// threshold pivoting for the static-column kernel (100 = classic partial pivoting;
+// 50 measured 3 % slower at S = 28: the extra ballot/shuffle outweighs skipped swaps)
+#ifndef NS_TAU_PCT
+#define NS_TAU_PCT 100
+#endif
 #ifndef HAFB_PSYNC
 #define HAFB_PSYNC 1
 #endif
@@ -102,12 +107,6 @@ constexpr int kDMax = 31;
 #endif
 #ifndef HAFB_CPRE
 #define HAFB_CPRE 0
-#endif
-#ifndef NS_SHFLROW
-#define NS_SHFLROW 0
-#endif
-#ifndef NS_PUBPRED
-#define NS_PUBPRED 0
 #endif
 #ifndef HAFB_NS_HI
 #define HAFB_NS_HI 32
@@ -602,6 +601,7 @@ __device__ __forceinline__ void ns_read(const cd (&w)[S], int b, cd& v) {
     }
 }
 
+
 template <int S, int W>
 __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const TeamCtx<W>& tc, cd* ws) {
     static_assert(W == 32 || W == 64, "NS variant: one or two warps per subset");
@@ -611,6 +611,7 @@ __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const Team
     cd* mus = ws + L::MU;  // multiplier of each logical row
     const int lane = tc.lane;
     cd hj = w[0], hn = w[1];
+    HT_DECL
 #pragma unroll 1
     for (int J = 0; J < S - 2; ++J) {
         const double key = (myrow > J && myrow < S) ? fabs(hj.re) + fabs(hj.im) : 0.0;
@@ -628,6 +629,19 @@ __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const Team
 #endif
         unsigned mx = __reduce_max_sync(0xffffffffu, (kb & ~63u) | (unsigned)(63 - lane));
         int wl = 63 - (int)(mx & 63u);
+#if NS_TAU_PCT < 100
+        if constexpr (W == 32) {
+            // threshold partial pivoting: keep the natural pivot row J+1 when its entry is
+            // within NS_TAU of the column maximum (multipliers stay below 1/NS_TAU): no swap
+            const unsigned nb = __ballot_sync(0xffffffffu, myrow == J + 1);
+            const int nl = nb ? __ffs(nb) - 1 : 0;
+            const double nk = __shfl_sync(0xffffffffu, key, nl);
+            if (nb && nk > 0.0 && nk * 100.0 >= (double)NS_TAU_PCT * __hiloint2double((int)(mx & ~63u), 0)) {
+                wl = nl;
+                mx = (mx & ~63u) | (unsigned)(63 - nl);
+            }
+        }
+#endif
 #if NS_SPECINV
         cd ip;
 #endif
@@ -652,6 +666,7 @@ __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const Team
             brow = (int)(second ? a1.im : a0.im);
             ip = second ? R[3] : R[1];
         }
+        HT_MARK(8);
         const int CS = (J * (J + 3)) / 2;  // column J in the packed store
         if ((mx & ~63u) == 0u) {  // nothing to eliminate below the subdiagonal: no update
             if (myrow <= J + 1) Hs[CS + myrow] = hj;
@@ -681,20 +696,11 @@ __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const Team
         if (myrow <= J + 1) Hs[CS + myrow] = hj;
         // column swap J+1 <-> brow: column J+1 is hn, column brow >= J+2 sits at w[brow]
         if (brow != J + 1) ns_xchg<S, 2, S>(w, brow, hn);
-        // publish the pivot row (logical row J+1): predicated stores, no per-column branch
-        const bool pl = lane == wl;
-#if NS_SHFLROW
-        (void)pl;
-#elif NS_PUBPRED
-        if (pl) pr[J + 1] = hn;
-        static_for<2, S>([&](auto cc) {
-            constexpr int c = decltype(cc)::value;
-            if (pl) pr[c] = w[c];
-            return true;
-        });
-#else
-        if (pl) {
-            pr[J + 1] = hn;
+        // publish the pivot row (logical row J+1): its lane stores columns J+1 .. S-1, one
+        // exit test per pair (measured alternatives: stores predicated over every column
+        // +10 %; a jump into a straight run of stores +5 %; register shuffles of the pivot
+        // row inside the sweep +3-5 %)
+        if (lane == wl) {
             static_for<0, S - 2, 2>([&](auto ii) {
                 constexpr int c = S - 1 - decltype(ii)::value;
                 pr[c] = w[c];
@@ -702,40 +708,14 @@ __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const Team
                 if (c - 1 <= J + 2) return false;
                 return true;
             });
+            pr[J + 1] = hn;
         }
-#endif
         tc.sync();
+        HT_MARK(10);
         // sweep, columns S-1 down to J+2: row update fused with the column gemv; at J+2
         // stash the next step's column J+2 and finish column J+1 (the gemv target)
         cd acc0 = mk(0.0, 0.0), acc1 = mk(0.0, 0.0);
-#if NS_SHFLROW
-        // pivot-row entries by register shuffle from the pivot lane (its row is not updated)
-        auto pbc = [&](const cd& v) -> cd {
-            cd r;
-            r.re = __shfl_sync(0xffffffffu, v.re, wl);
-            r.im = __shfl_sync(0xffffffffu, v.im, wl);
-            return r;
-        };
-        const cd p1 = pbc(hn);
-        cd pa = pbc(w[S - 1]), ma = mus[S - 1];
-        static_for<0, S - 2>([&](auto ii) {
-            constexpr int c = S - 1 - decltype(ii)::value;
-            const cd pn = c - 1 >= 2 ? pbc(w[c - 1 >= 2 ? c - 1 : 2]) : p1;
-            const cd mn = mus[c - 1];
-            w[c] = f_cms(w[c], mu, pa);
-            if constexpr (c & 1) acc1 = f_cma(acc1, ma, w[c]);
-            else acc0 = f_cma(acc0, ma, w[c]);
-            pa = pn;
-            ma = mn;
-            if (c == J + 2) {
-                const cd nh = w[c];
-                hj = f_add(f_cms(hn, mu, p1), f_add(acc0, acc1));
-                hn = nh;
-                return false;
-            }
-            return true;
-        });
-#elif NS_PAIR
+#if NS_PAIR
         // columns in pairs (c, c-1) under one exit test: the pair that holds J+2 may also
         // hold J+1, whose register copy is dead (it travels in hn) and whose multiplier is
         // zero, so updating it is harmless
@@ -780,6 +760,7 @@ __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const Team
             return true;
         });
 #endif
+        HT_MARK(11);
     }
     // logical columns S-2 (hj) and S-1 (hn): every row
     if (myrow < S) {

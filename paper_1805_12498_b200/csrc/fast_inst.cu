@@ -13,10 +13,12 @@ namespace hafb {
 // Hessenberg variant per size (measured on B200, tools/micro/phase.cu and
 // tools/class_time.py under ncu):
 //   18 <= S <= 32  static-column register reduction (ns_hessenberg, one warp per subset);
+//   S = 34, 36     (no loops) one warp with the extra rows held column-wise (nsx_hessenberg);
 //   S >= 34        shared-memory reduction over 64-lane teams (smem_hessenberg: a two-warp
 //                  static-column team measured 7-11 % slower -- its second warp carries
 //                  2..8 rows but issues the whole instruction stream);
-//   S <= 16        register-window reduction (fast_hessenberg, 16-lane teams).
+//   10 <= S <= 16  the same static-column kernel on 16-lane teams (two subsets per warp);
+//   S <= 8         register-window reduction (fast_hessenberg, 2..8-lane teams).
 #ifndef HAFB_SMEM_HI
 #define HAFB_SMEM_HI 34
 #endif
@@ -32,11 +34,14 @@ constexpr bool smem_hess(int S) { return !ns_variant(S) && ((S >= 18 && S <= 24)
 #ifndef HAFB_NS_WIDE_THREADS
 #define HAFB_NS_WIDE_THREADS 64
 #endif
+#ifndef HAFB_NS_SMALL_THREADS
+#define HAFB_NS_SMALL_THREADS 512
+#endif
 #ifndef HAFB_REG_THREADS
 #define HAFB_REG_THREADS 384
 #endif
 constexpr int threads_for(int S) {
-    return ns_variant(S) ? (S > 32 ? HAFB_NS_WIDE_THREADS : S <= 22 ? 512 : HAFB_REG_THREADS)
+    return ns_variant(S) ? (S > 32 ? HAFB_NS_WIDE_THREADS : S <= 16 ? kFastThreads : S <= 22 ? HAFB_NS_SMALL_THREADS : HAFB_REG_THREADS)
            : !smem_hess(S) && S >= 26 ? (S > 32 ? 256 : HAFB_REG_THREADS)
            : S > 32 ? 64  // 64-lane teams: one team per block (register-limited: 5 teams/SM, not 4)
            : smem_hess(S) ? 32  // one team per block: the register file packs one more team

@@ -83,7 +83,7 @@ constexpr int kDMax = 31;
 #define HAFB_NS 1
 #endif
 #ifndef HAFB_NS_LO
-#define HAFB_NS_LO 18
+#define HAFB_NS_LO 10
 #endif
 #ifndef NS_SPECINV
 #define NS_SPECINV 1
@@ -604,7 +604,10 @@ __device__ __forceinline__ void ns_read(const cd (&w)[S], int b, cd& v) {
 
 template <int S, int W>
 __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const TeamCtx<W>& tc, cd* ws) {
-    static_assert(W == 32 || W == 64, "NS variant: one or two warps per subset");
+    static_assert(W == 16 || W == 32 || W == 64, "NS variant: half-warp, one- or two-warp teams");
+    // W = 16: two teams per warp (team mask / lane base); their uniform branches may diverge
+    const unsigned tm = W < 32 ? tc.wmask : 0xffffffffu;
+    const int tb = W < 32 ? ((int)(threadIdx.x & 31) & ~(W - 1)) : 0;
     using L = FastLayout<S>;
     cd* Hs = ws + L::HS;
     cd* pr = ws + L::PR;  // pivot row, by logical column
@@ -627,15 +630,15 @@ __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const Team
 #else
         const unsigned kb = key > 0.0 ? __float_as_uint(__double2float_ru(key)) : 0u;
 #endif
-        unsigned mx = __reduce_max_sync(0xffffffffu, (kb & ~63u) | (unsigned)(63 - lane));
+        unsigned mx = __reduce_max_sync(tm, (kb & ~63u) | (unsigned)(63 - lane));
         int wl = 63 - (int)(mx & 63u);
 #if NS_TAU_PCT < 100
-        if constexpr (W == 32) {
+        if constexpr (W <= 32) {
             // threshold partial pivoting: keep the natural pivot row J+1 when its entry is
             // within NS_TAU of the column maximum (multipliers stay below 1/NS_TAU): no swap
-            const unsigned nb = __ballot_sync(0xffffffffu, myrow == J + 1);
+            const unsigned nb = __ballot_sync(tm, myrow == J + 1) >> tb;
             const int nl = nb ? __ffs(nb) - 1 : 0;
-            const double nk = __shfl_sync(0xffffffffu, key, nl);
+            const double nk = __shfl_sync(tm, key, tb + nl);
             if (nb && nk > 0.0 && nk * 100.0 >= (double)NS_TAU_PCT * __hiloint2double((int)(mx & ~63u), 0)) {
                 wl = nl;
                 mx = (mx & ~63u) | (unsigned)(63 - nl);
@@ -675,10 +678,10 @@ __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const Team
             continue;
         }
 #if NS_SPECINV
-        if constexpr (W == 32) {
-            brow = __shfl_sync(0xffffffffu, myrow, wl);
-            ip.re = __shfl_sync(0xffffffffu, myinv.re, wl);
-            ip.im = __shfl_sync(0xffffffffu, myinv.im, wl);
+        if constexpr (W <= 32) {
+            brow = __shfl_sync(tm, myrow, tb + wl);
+            ip.re = __shfl_sync(tm, myinv.re, tb + wl);
+            ip.im = __shfl_sync(tm, myinv.im, tb + wl);
         }
 #else
         static_assert(W == 32, "the two-warp NS variant needs NS_SPECINV");

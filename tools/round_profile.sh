@@ -10,3 +10,5 @@ timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_d
   -k "regex:fast_term_kernel" --csv --log-file gpurun_out/dram_$TAG.csv python tools/class_time.py fast > /dev/null 2>&1; echo "dram rc=$?"
 timeout 600 ncu --set full --import-source on --clock-control none --kernel-name-base demangled \
   -k "regex:fast_term_kernel<.int.28," -c 1 -o gpurun_out/ncu_full_S28_$TAG python tools/class_time.py fast > /dev/null 2>&1; echo "full rc=$?"
+timeout 600 python bench.py --n 56 --steps 2 --warmup 3 --mirror-steps 0 > gpurun_out/bench_n56_$TAG.log 2>&1; echo "n56 rc=$?"
+timeout 300 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref_$TAG.log 2>&1; echo "ref rc=$?"

@@ -134,7 +134,8 @@ struct FastLayout {
     static constexpr int FLAG = G + kDMax + 2;        // [1]
     static constexpr int SIGN = (S + 3) / 4 + 1;      // cd slots holding S ints
     static constexpr int SIG = FLAG + 2;              // [2][S] int: logical row -> lane (SH)
-    static constexpr int TOTAL = SIG + 2 * SIGN;
+    static constexpr int CRN = SIG + 2 * SIGN;        // NSX: the extra rows' columns >= 32 ([E][E])
+    static constexpr int TOTAL = CRN + (S > 32 ? (S - 32) * (S - 32) : 0);
 };
 
 template <int W>
@@ -774,37 +775,44 @@ __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const Team
 
 
 // ============================================================================ NSX variant
-// S = 32 + E (E = 2, 4): one warp per subset.  Rows 0..31 are lane rows exactly as in
+// S = 32 + E (E = 2..8): one warp per subset.  Rows 0..31 are lane rows exactly as in
 // ns_hessenberg; the E extra rows are held COLUMN-wise: lane l keeps their entries of
-// columns l (slot 0) and 32 + l (slot 1, lanes < E), so no second warp idles on E rows.
-// Per step the extra rows cost: their pivot candidates (lane J & 31), a shuffle pair for
+// column l in registers, and their E x E corner (columns 32..S-1) lives in shared memory
+// (lanes < E update it), so no second warp idles on E rows.  Per step the extra rows
+// cost: their pivot candidates (lane J & 31), a shuffle pair (or a corner exchange) for
 // the column swap, an E-row rank-1 update + gemv partial per lane, and one butterfly
 // all-reduce of the E gemv partials.  Same arithmetic identities as ns_hessenberg.
 #ifndef HAFB_NSX
 #define HAFB_NSX 1
 #endif
-constexpr bool nsx_variant(int S) { return HAFB_NSX && (S == 34 || S == 36); }
-
-template <int E>
-__device__ __forceinline__ cd nsx_slot(const cd (&x)[2], bool hi) { return hi ? x[1] : x[0]; }
+#ifndef HAFB_NSX_HI
+#define HAFB_NSX_HI 38
+#endif
+constexpr bool nsx_variant(int S) { return HAFB_NSX && S >= 34 && S <= HAFB_NSX_HI; }
 
 template <int S>
-__device__ __forceinline__ void nsx_hessenberg(cd (&w)[S], cd (&ex)[S - 32][2], int& myrow,
+__device__ __forceinline__ void nsx_hessenberg(cd (&w)[S], cd (&ex)[S - 32], int& myrow,
                                                int (&elab)[S - 32], const TeamCtx<32>& tc, cd* ws) {
     constexpr int E = S - 32;
-    using L = FastLayout<S>;
+    using L = FastLayout<S, false, false>;  // NSX runs without loops: the kernel's layout
     cd* Hs = ws + L::HS;
     cd* pr = ws + L::PR;
     cd* mus = ws + L::MU;
+    cd* CR = ws + L::CRN;  // CR[e * E + q] = h(32 + e, 32 + q)
     const int lane = tc.lane;
     cd hj = w[0], hn = w[1];
+    __syncwarp();
 #pragma unroll 1
     for (int J = 0; J < S - 2; ++J) {
         const int jl = J & 31;
-        const bool js = J >= 32;
         cd xv[E];  // extra rows' column-J entries (meaningful in lane jl)
+        if (J >= 32) {
 #pragma unroll
-        for (int e = 0; e < E; ++e) xv[e] = js ? ex[e][1] : ex[e][0];
+            for (int e = 0; e < E; ++e) xv[e] = CR[e * E + (J - 32)];
+        } else {
+#pragma unroll
+            for (int e = 0; e < E; ++e) xv[e] = ex[e];
+        }
         const double key = (myrow > J && myrow < S) ? fabs(hj.re) + fabs(hj.im) : 0.0;
         const cd myinv = f_inv(hj);
         unsigned pk = ((unsigned)__double2hiint(key) & ~63u) | (unsigned)(63 - lane);
@@ -867,38 +875,38 @@ __device__ __forceinline__ void nsx_hessenberg(cd (&w)[S], cd (&ex)[S - 32][2], 
                 if (elab[e] <= J + 1) Hs[CS + elab[e]] = xv[e];
             }
         }
-        // column swap J+1 <-> brow: lane rows by the register tree; extra rows by lanes
+        // column swap J+1 <-> brow: lane rows by the register tree; extra rows by a
+        // shuffle pair (both columns < 32) or a corner exchange
         if (brow != J + 1) {
             ns_xchg<S, 2, S>(w, brow, hn);
-            const int a = (J + 1) & 31, b = brow & 31;
-            const bool sa = J + 1 >= 32, sb = brow >= 32;
-            if (a == b) {  // same lane, the two slots
-                if (lane == a) {
-#pragma unroll
-                    for (int e = 0; e < E; ++e) {
-                        const cd t = ex[e][0];
-                        ex[e][0] = ex[e][1];
-                        ex[e][1] = t;
-                    }
-                }
-            } else {
+            const int a = J + 1, b = brow;  // a < b
+            if (b < 32) {
                 const int src = lane == a ? b : a;
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
-                    const cd out = lane == a ? (sa ? ex[e][1] : ex[e][0]) : (sb ? ex[e][1] : ex[e][0]);
                     cd in;
-                    in.re = __shfl_sync(0xffffffffu, out.re, src);
-                    in.im = __shfl_sync(0xffffffffu, out.im, src);
-                    if (lane == a) {
-                        if (sa) ex[e][1] = in;
-                        else ex[e][0] = in;
-                    }
-                    if (lane == b) {
-                        if (sb) ex[e][1] = in;
-                        else ex[e][0] = in;
+                    in.re = __shfl_sync(0xffffffffu, ex[e].re, src);
+                    in.im = __shfl_sync(0xffffffffu, ex[e].im, src);
+                    if (lane == a || lane == b) ex[e] = in;
+                }
+            } else if (a < 32) {
+                if (lane == a) {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        const cd t = ex[e];
+                        ex[e] = CR[e * E + (b - 32)];
+                        CR[e * E + (b - 32)] = t;
                     }
                 }
+            } else if (lane == 0) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const cd t = CR[e * E + (a - 32)];
+                    CR[e * E + (a - 32)] = CR[e * E + (b - 32)];
+                    CR[e * E + (b - 32)] = t;
+                }
             }
+            __syncwarp();
         }
         // publish the pivot row (logical row J+1) by logical column
         if (pw < 32) {
@@ -912,15 +920,13 @@ __device__ __forceinline__ void nsx_hessenberg(cd (&w)[S], cd (&ex)[S - 32][2], 
                 });
             }
         } else {
-            cd r0 = ex[0][0], r1 = ex[0][1];
+            const int es = pw - 32;
+            cd r0 = ex[0];
 #pragma unroll
             for (int e = 1; e < E; ++e)
-                if (pw - 32 == e) {
-                    r0 = ex[e][0];
-                    r1 = ex[e][1];
-                }
+                if (es == e) r0 = ex[e];
             pr[lane] = r0;
-            if (lane < E) pr[32 + lane] = r1;
+            if (lane < E) pr[32 + lane] = CR[es * E + lane];
         }
         __syncwarp();
         cd mue[E];
@@ -951,16 +957,22 @@ __device__ __forceinline__ void nsx_hessenberg(cd (&w)[S], cd (&ex)[S - 32][2], 
         cd part[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) part[e] = mk(0.0, 0.0);
+        if (lane >= J + 1) {
+            const cd pc = pr[lane], mc = mus[lane];
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            const int c = lane + 32 * q;
-            if ((q == 0 || lane < E) && c >= J + 1) {
-                const cd pc = pr[c], mc = mus[c];
+            for (int e = 0; e < E; ++e) {
+                ex[e] = f_cms(ex[e], mue[e], pc);
+                part[e] = f_cma(part[e], mc, ex[e]);
+            }
+        }
+        if (lane < E && 32 + lane >= J + 1) {
+            const cd pc = pr[32 + lane], mc = mus[32 + lane];
 #pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    ex[e][q] = f_cms(ex[e][q], mue[e], pc);
-                    part[e] = f_cma(part[e], mc, ex[e][q]);
-                }
+            for (int e = 0; e < E; ++e) {
+                cd v = CR[e * E + lane];
+                v = f_cms(v, mue[e], pc);
+                part[e] = f_cma(part[e], mc, v);
+                CR[e * E + lane] = v;
             }
         }
 #pragma unroll
@@ -971,23 +983,28 @@ __device__ __forceinline__ void nsx_hessenberg(cd (&w)[S], cd (&ex)[S - 32][2], 
                 part[e].im += __shfl_xor_sync(0xffffffffu, part[e].im, off);
             }
         }
-        // column J+1 of the extra rows (lane (J+1) & 31, its slot): += gemv
-        if (lane == ((J + 1) & 31)) {
-            const bool s1 = J + 1 >= 32;
+        // column J+1 of the extra rows += gemv (its owner: lane J+1, or corner lane J+1-32)
+        if (J + 1 < 32) {
+            if (lane == J + 1) {
 #pragma unroll
-            for (int e = 0; e < E; ++e) {
-                if (s1) ex[e][1] = f_add(ex[e][1], part[e]);
-                else ex[e][0] = f_add(ex[e][0], part[e]);
+                for (int e = 0; e < E; ++e) ex[e] = f_add(ex[e], part[e]);
             }
+        } else if (lane == J + 1 - 32) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) CR[e * E + lane] = f_add(CR[e * E + lane], part[e]);
         }
+        __syncwarp();
     }
-    // logical columns S-2 and S-1: every row
+    // logical columns S-2 and S-1 (both >= 32): every row
     Hs[((S - 2) * (S + 1)) / 2 + myrow] = hj;
     Hs[((S - 1) * (S + 2)) / 2 + myrow] = hn;
-    if (lane == ((S - 2) & 31) || lane == ((S - 1) & 31)) {
-        const int c = 32 + lane;  // both are slot-1 columns (S - 2 >= 32)
+    if (lane < E) {
+        const int e = lane;
 #pragma unroll
-        for (int e = 0; e < E; ++e) Hs[(c * (c + 3)) / 2 + elab[e]] = ex[e][1];
+        for (int q = E - 2; q < E; ++q) {
+            const int c = 32 + q;
+            Hs[(c * (c + 3)) / 2 + elab[e]] = CR[e * E + q];
+        }
     }
 }
 
@@ -1147,11 +1164,12 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
             smem_hessenberg<S, W, LOOPS>(H, myrow, tc, ws);
         } else if constexpr (NSX) {
             constexpr int E = S - 32;
-            cd ex[E > 0 ? E : 1][2];
+            cd ex[E > 0 ? E : 1];
             int elab[E > 0 ? E : 1];
-            // extra rows 32+e (vertices 2 v_{16+e/2} + (e&1), pair-swapped rows of Atilde),
-            // columns lane and 32+lane (vertices 2 v_{c/2} + (c&1))
+            // extra rows 32+e (vertices 2 v_{16+e/2} + (e&1), pair-swapped rows of Atilde):
+            // column lane in registers, columns 32+q (q < E) in the shared-memory corner
             const int cb1 = lane < E ? (int)__fns(ir.mask, 0, 16 + (lane >> 1) + 1) : 0;
+            cd* CR = ws + L::CRN;
             gather([&](const cd* src, int ld) {
                 static_for<0, S>([&](auto c) {
                     const int vc = 2 * vbit[c() >> 1] + (c() & 1);
@@ -1161,8 +1179,8 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
                 static_for<0, E>([&](auto ee) {
                     constexpr int e = decltype(ee)::value;
                     const int rv = 2 * vbit[16 + e / 2] + (e & 1);
-                    ex[e][0] = src[rv * ld + 2 * mybit + (lane & 1)];
-                    ex[e][1] = lane < E ? src[rv * ld + 2 * cb1 + (lane & 1)] : mk(0.0, 0.0);
+                    ex[e] = src[rv * ld + 2 * mybit + (lane & 1)];
+                    if (lane < E) CR[e * E + lane] = src[rv * ld + 2 * cb1 + (lane & 1)];
                     elab[e] = 32 + e;
                     return true;
                 });
@@ -1236,22 +1254,19 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
                     prev.re = tshfl_up<W>(P[k - 1].re, 1);
                     prev.im = tshfl_up<W>(P[k - 1].im, 1);
                     if (lane == 0) prev = mk(0.0, 0.0);
-                    cd acc = f_cms(prev, cfk[k - 1], P[k - 1]);
-                    cd acc2 = mk(0.0, 0.0), acc3 = mk(0.0, 0.0), acc4 = mk(0.0, 0.0);
-                    static_for<1, k, 4>([&](auto ii) {
-                        constexpr int i0 = decltype(ii)::value;
-                        if (i0 >= k + opaque_zero) return false;
-                        static_for<i0, (i0 + 4 < k ? i0 + 4 : k)>([&](auto jj) {
-                            constexpr int i = decltype(jj)::value;
-                            if constexpr ((i & 3) == 0) acc = f_cms(acc, cfk[i - 1], P[i - 1]);
-                            else if constexpr ((i & 3) == 1) acc2 = f_cms(acc2, cfk[i - 1], P[i - 1]);
-                            else if constexpr ((i & 3) == 2) acc3 = f_cms(acc3, cfk[i - 1], P[i - 1]);
-                            else acc4 = f_cms(acc4, cfk[i - 1], P[i - 1]);
-                            return true;
-                        });
+                    // older terms (P_l, l <= k-2) in accumulators independent of P_{k-1}:
+                    // without a per-step barrier they overlap the previous step's chain
+                    cd acc1 = mk(0.0, 0.0), acc2 = mk(0.0, 0.0), acc3 = mk(0.0, 0.0), acc4 = mk(0.0, 0.0);
+                    static_for<1, k>([&](auto jj) {
+                        constexpr int i = decltype(jj)::value;
+                        if constexpr ((i & 3) == 0) acc1 = f_cms(acc1, cfk[i - 1], P[i - 1]);
+                        else if constexpr ((i & 3) == 1) acc2 = f_cms(acc2, cfk[i - 1], P[i - 1]);
+                        else if constexpr ((i & 3) == 2) acc3 = f_cms(acc3, cfk[i - 1], P[i - 1]);
+                        else acc4 = f_cms(acc4, cfk[i - 1], P[i - 1]);
                         return true;
                     });
-                    acc = f_add(f_add(acc, acc2), f_add(acc3, acc4));
+                    cd acc = f_cms(prev, cfk[k - 1], P[k - 1]);
+                    acc = f_add(acc, f_add(f_add(acc1, acc2), f_add(acc3, acc4)));
                     if constexpr (k < S) P[k] = acc;
                     else if (lane < S) A[lane] = acc;
                     return true;

@@ -374,9 +374,9 @@ def test_fast_terms_every_size_vs_oracle(S):
     assert np.abs(got - ref).max() <= 1e-10 * scale
 
 
-@pytest.mark.parametrize("S", [34, 36])
+@pytest.mark.parametrize("S", [34, 36, 38])
 def test_fast_extra_row_classes_full_class_vs_oracle(S):
-    """S = 34, 36 run one-warp teams with the rows beyond 32 held column-wise (NSX).
+    """S = 34..38 run one-warp teams with the rows beyond 32 held column-wise (NSX).
     Every subset of the class for n = 44 (C(22, S/2) masks, thousands of teams walking
     long mask runs): no failing status, every term within 1e-10 of the largest oracle
     term, and a seeded sample checked per term against the bit-exact oracle."""

@@ -5,7 +5,7 @@ from oracle import oracle as O
 A = W.cfg4(3, 52)
 at, dg, nh = engine._prepare(A, False)
 D = nh
-for m in (17, 18):
+for m in (17, 18, 19):
     # all masks of popcount m below 2^D, in chunks
     from math import comb
     bad = []

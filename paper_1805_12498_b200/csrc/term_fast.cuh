@@ -790,6 +790,49 @@ __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const Team
 #endif
 constexpr bool nsx_variant(int S) { return HAFB_NSX && S >= 34 && S <= HAFB_NSX_HI; }
 
+
+// sum of v[0..E) over the warp into every lane (E <= 8): reduce-scatter + butterfly + gather
+template <int E>
+__device__ __forceinline__ void nsx_allreduce(cd (&v)[E], int lane) {
+    constexpr int P = E <= 1 ? 1 : E <= 2 ? 2 : E <= 4 ? 4 : 8;  // padded length
+    constexpr int LG = P == 1 ? 0 : P == 2 ? 1 : P == 4 ? 2 : 3;
+    cd x[P];
+#pragma unroll
+    for (int e = 0; e < P; ++e) x[e] = e < E ? v[e] : mk(0.0, 0.0);
+    // level l (off = 16 >> l): keep half h = lane bit; x[0..len/2) <- x[h-half] + partner's
+#pragma unroll
+    for (int l = 0; l < LG; ++l) {
+        const int off = 16 >> l;
+        const int len = P >> l, half = len >> 1;
+        const bool up = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < half; ++i) {
+            const cd keep = up ? x[half + i] : x[i];
+            const cd send = up ? x[i] : x[half + i];
+            cd r;
+            r.re = __shfl_xor_sync(0xffffffffu, send.re, off);
+            r.im = __shfl_xor_sync(0xffffffffu, send.im, off);
+            x[i] = f_add(keep, r);
+        }
+    }
+    // x[0] now holds a partial of element idx = bits of lane at 16, 8, ... (LG bits)
+#pragma unroll
+    for (int off = 16 >> LG; off > 0; off >>= 1) {
+        x[0].re += __shfl_xor_sync(0xffffffffu, x[0].re, off);
+        x[0].im += __shfl_xor_sync(0xffffffffu, x[0].im, off);
+    }
+    // element e's total sits in the lanes whose top LG bits spell e (MSB first = level 0)
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        int src = 0;
+#pragma unroll
+        for (int l = 0; l < LG; ++l)
+            if ((e >> (LG - 1 - l)) & 1) src |= 16 >> l;
+        v[e].re = __shfl_sync(0xffffffffu, x[0].re, src);
+        v[e].im = __shfl_sync(0xffffffffu, x[0].im, src);
+    }
+}
+
 template <int S>
 __device__ __forceinline__ void nsx_hessenberg(cd (&w)[S], cd (&ex)[S - 32], int& myrow,
                                                int (&elab)[S - 32], const TeamCtx<32>& tc, cd* ws) {
@@ -975,14 +1018,10 @@ __device__ __forceinline__ void nsx_hessenberg(cd (&w)[S], cd (&ex)[S - 32], int
                 CR[e * E + lane] = v;
             }
         }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-                part[e].re += __shfl_xor_sync(0xffffffffu, part[e].re, off);
-                part[e].im += __shfl_xor_sync(0xffffffffu, part[e].im, off);
-            }
-        }
+        // all-reduce of the E partials: reduce-scatter (each level halves the vector a lane
+        // keeps: lanes with bit `off` set keep the upper half), a butterfly over the
+        // remaining levels, then every lane fetches the E totals
+        nsx_allreduce<E>(part, lane);
         // column J+1 of the extra rows += gemv (its owner: lane J+1, or corner lane J+1-32)
         if (J + 1 < 32) {
             if (lane == J + 1) {

@@ -99,6 +99,9 @@ constexpr int kDMax = 31;
 #ifndef NS_TAU_PCT
 #define NS_TAU_PCT 100
 #endif
+#ifndef NS_BRANCHLESS
+#define NS_BRANCHLESS 1
+#endif
 #ifndef HAFB_PSYNC
 #define HAFB_PSYNC 1
 #endif
@@ -695,8 +698,19 @@ __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const Team
         if (myrow == brow) myrow = J + 1;
         else if (myrow == J + 1) myrow = brow;
         const bool elim = myrow >= J + 2 && myrow < S;
+#if NS_BRANCHLESS
+        // selects and predicated stores: no divergent region (BSSY/BSYNC) on the chain
+        const cd mprod = f_mul(hj, ip);
+        const cd mu = mk(elim ? mprod.re : 0.0, elim ? mprod.im : 0.0);
+        if constexpr (S >= W) {
+            mus[myrow] = mu;
+        } else {
+            if (myrow < S) mus[myrow] = mu;
+        }
+#else
         const cd mu = elim ? f_mul(hj, ip) : mk(0.0, 0.0);
         if (myrow < S) mus[myrow] = mu;
+#endif
         if (myrow <= J + 1) Hs[CS + myrow] = hj;
         // column swap J+1 <-> brow: column J+1 is hn, column brow >= J+2 sits at w[brow]
         if (brow != J + 1) ns_xchg<S, 2, S>(w, brow, hn);
@@ -704,6 +718,21 @@ __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const Team
         // exit test per pair (measured alternatives: stores predicated over every column
         // +10 %; a jump into a straight run of stores +5 %; register shuffles of the pivot
         // row inside the sweep +3-5 %)
+#if NS_BRANCHLESS
+        {
+            // warp-uniform exit test per pair of columns around stores predicated on the
+            // pivot lane: no divergent region
+            const bool pl = lane == wl;
+            static_for<0, S - 2, 2>([&](auto ii) {
+                constexpr int c = S - 1 - decltype(ii)::value;
+                if (pl) pr[c] = w[c];
+                if (c - 1 >= J + 2 && pl) pr[c - 1] = w[c - 1];
+                if (c - 1 <= J + 2) return false;
+                return true;
+            });
+            if (pl) pr[J + 1] = hn;
+        }
+#else
         if (lane == wl) {
             static_for<0, S - 2, 2>([&](auto ii) {
                 constexpr int c = S - 1 - decltype(ii)::value;
@@ -714,6 +743,7 @@ __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const Team
             });
             pr[J + 1] = hn;
         }
+#endif
         tc.sync();
         HT_MARK(10);
         // sweep, columns S-1 down to J+2: row update fused with the column gemv; at J+2
@@ -859,13 +889,12 @@ __device__ __forceinline__ void nsx_hessenberg(cd (&w)[S], cd (&ex)[S - 32], int
         const double key = (myrow > J && myrow < S) ? fabs(hj.re) + fabs(hj.im) : 0.0;
         const cd myinv = f_inv(hj);
         unsigned pk = ((unsigned)__double2hiint(key) & ~63u) | (unsigned)(63 - lane);
-        if (lane == jl) {
+        const bool pj = lane == jl;  // the lane holding the extra rows' column J
 #pragma unroll
-            for (int e = 0; e < E; ++e) {
-                const double kx = elab[e] > J ? fabs(xv[e].re) + fabs(xv[e].im) : 0.0;
-                const unsigned c = ((unsigned)__double2hiint(kx) & ~63u) | (unsigned)(63 - (32 + e));
-                pk = c > pk ? c : pk;
-            }
+        for (int e = 0; e < E; ++e) {
+            const double kx = (pj && elab[e] > J) ? fabs(xv[e].re) + fabs(xv[e].im) : 0.0;
+            const unsigned c = ((unsigned)__double2hiint(kx) & ~63u) | (unsigned)(63 - (32 + e));
+            pk = c > pk ? c : pk;
         }
         const unsigned mx = __reduce_max_sync(0xffffffffu, pk);
         const int pw = 63 - (int)(mx & 63u);  // physical pivot row (>= 32: an extra row)
@@ -908,15 +937,16 @@ __device__ __forceinline__ void nsx_hessenberg(cd (&w)[S], cd (&ex)[S - 32], int
         for (int e = 0; e < E; ++e) elab[e] = elab[e] == brow ? J + 1 : (elab[e] == J + 1 ? brow : elab[e]);
         // multipliers of every logical row (all S rewritten each step) and column J's store
         const bool elim = myrow >= J + 2 && myrow < S;
-        const cd mu = elim ? f_mul(hj, ip) : mk(0.0, 0.0);
+        const cd mprod = f_mul(hj, ip);
+        const cd mu = mk(elim ? mprod.re : 0.0, elim ? mprod.im : 0.0);
         mus[myrow] = mu;
         if (myrow <= J + 1) Hs[CS + myrow] = hj;
-        if (lane == jl) {
 #pragma unroll
-            for (int e = 0; e < E; ++e) {
-                mus[elab[e]] = elab[e] >= J + 2 ? f_mul(xv[e], ip) : mk(0.0, 0.0);
-                if (elab[e] <= J + 1) Hs[CS + elab[e]] = xv[e];
-            }
+        for (int e = 0; e < E; ++e) {  // stores predicated on lane jl (no divergent region)
+            const cd xp = f_mul(xv[e], ip);
+            const bool ee = elab[e] >= J + 2;
+            if (pj) mus[elab[e]] = mk(ee ? xp.re : 0.0, ee ? xp.im : 0.0);
+            if (pj && elab[e] <= J + 1) Hs[CS + elab[e]] = xv[e];
         }
         // column swap J+1 <-> brow: lane rows by the register tree; extra rows by a
         // shuffle pair (both columns < 32) or a corner exchange
@@ -953,15 +983,15 @@ __device__ __forceinline__ void nsx_hessenberg(cd (&w)[S], cd (&ex)[S - 32], int
         }
         // publish the pivot row (logical row J+1) by logical column
         if (pw < 32) {
-            if (lane == pw) {
-                pr[J + 1] = hn;
-                static_for<0, S - 2>([&](auto ii) {
-                    constexpr int c = S - 1 - decltype(ii)::value;
-                    if (c < J + 2) return false;
-                    pr[c] = w[c];
-                    return true;
-                });
-            }
+            const bool pl = lane == pw;
+            static_for<0, S - 2, 2>([&](auto ii) {
+                constexpr int c = S - 1 - decltype(ii)::value;
+                if (pl) pr[c] = w[c];
+                if (c - 1 >= J + 2 && pl) pr[c - 1] = w[c - 1];
+                if (c - 1 <= J + 2) return false;
+                return true;
+            });
+            if (pl) pr[J + 1] = hn;
         } else {
             const int es = pw - 32;
             cd r0 = ex[0];
@@ -1000,11 +1030,16 @@ __device__ __forceinline__ void nsx_hessenberg(cd (&w)[S], cd (&ex)[S - 32], int
         cd part[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) part[e] = mk(0.0, 0.0);
-        if (lane >= J + 1) {
-            const cd pc = pr[lane], mc = mus[lane];
+        {
+            // selects instead of a divergent region: a finished column keeps its (finite)
+            // value and contributes a zero coefficient
+            const bool live = lane >= J + 1;
+            const cd pc = pr[lane], mc0 = mus[lane];
+            const cd mc = mk(live ? mc0.re : 0.0, live ? mc0.im : 0.0);
 #pragma unroll
             for (int e = 0; e < E; ++e) {
-                ex[e] = f_cms(ex[e], mue[e], pc);
+                const cd nv = f_cms(ex[e], mue[e], pc);
+                ex[e] = mk(live ? nv.re : ex[e].re, live ? nv.im : ex[e].im);
                 part[e] = f_cma(part[e], mc, ex[e]);
             }
         }

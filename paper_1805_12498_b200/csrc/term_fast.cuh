@@ -1351,10 +1351,20 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
                 cd* cf = ws + L::CF + (k & 1) * S;
                 if constexpr (k >= 2) {
                     const cd beta = hget(k - 1, k - 2);  // h[k-1][k-2]
+#if NS_BRANCHLESS
+                    {  // select + predicated store: no divergent region per step
+                        const bool on = lane <= k - 2;
+                        const cd np = f_mul(lane == k - 2 ? mk(1.0, 0.0) : prodl, beta);
+                        prodl = mk(on ? np.re : prodl.re, on ? np.im : prodl.im);
+                        const cd v = f_mul(hget_mine(k - 1), prodl);
+                        if (on) cf[lane] = v;
+                    }
+#else
                     if (lane <= k - 2) {
                         prodl = f_mul(lane == k - 2 ? mk(1.0, 0.0) : prodl, beta);
                         cf[lane] = f_mul(hget_mine(k - 1), prodl);
                     }
+#endif
                     if constexpr (NSX && k >= 34) {  // rows 32 + lane of the extra coefficients
                         if (lane < S - 32 && 32 + lane <= k - 2) {
                             prodx = f_mul(32 + lane == k - 2 ? mk(1.0, 0.0) : prodx, beta);
@@ -1454,10 +1464,10 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
                     gm.im = __shfl_sync(tc.wmask, acc.im, src0 + m - 1) * sc;
                 }
                 const int j = k - m;
-                if (k <= D && j >= 1 && j <= S) {
-                    const double wgt = 0.5 * (double)(k + m);
-                    acc = f_cma(acc, A[S - j], mk(wgt * gm.re, wgt * gm.im));
-                }
+                const bool on = k <= D && j >= 1 && j <= S;
+                // zero weight instead of a divergent region (the index is clamped in range)
+                const double wgt = on ? 0.5 * (double)(k + m) : 0.0;
+                acc = f_cma(acc, A[S - (on ? j : 1)], mk(wgt * gm.re, wgt * gm.im));
             }
             if (lane < S + 1) {
                 const cd a = A[lane];

@@ -593,6 +593,7 @@ __device__ __forceinline__ void ns_xchg(cd (&w)[S], int b, cd& v) {
         else ns_xchg<S, MID, HI>(w, b, v);
     }
 }
+
 // v = w[b]
 template <int S, int LO, int HI>
 __device__ __forceinline__ void ns_read(const cd (&w)[S], int b, cd& v) {
@@ -713,7 +714,7 @@ __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const Team
 #endif
         if (myrow <= J + 1) Hs[CS + myrow] = hj;
         // column swap J+1 <-> brow: column J+1 is hn, column brow >= J+2 sits at w[brow]
-        if (brow != J + 1) ns_xchg<S, 2, S>(w, brow, hn);
+        if (brow != J + 1) ns_xchg<S, 2, S>(w, brow, hn);  // (a switch jump table: 6x slower)
         // publish the pivot row (logical row J+1): its lane stores columns J+1 .. S-1, one
         // exit test per pair (measured alternatives: stores predicated over every column
         // +10 %; a jump into a straight run of stores +5 %; register shuffles of the pivot

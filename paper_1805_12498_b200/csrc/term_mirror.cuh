@@ -146,12 +146,17 @@ __global__ void __launch_bounds__(kMirrorThreads) mirror_term_kernel(
     int* STOP = ints + 2 * S;   // [S+2] smallest i of coef chain k (k = 1..S)
     const int n = 2 * n_half;
     const int D = n_half;
-    const long long stride = (long long)gridDim.x * TPB;
+    // each team walks a contiguous run of the class's items (successive masks by Gosper's
+    // step, ItemCursor): which team computes which subset changes, no arithmetic does
+    const long long n_teams = (long long)gridDim.x * TPB;
+    const long long chunk = (ci.n_items + n_teams - 1) / n_teams;
+    const long long first = ((long long)blockIdx.x * TPB + tc.tib) * chunk;
+    ItemCursor cur;
 
-    for (long long base = (long long)blockIdx.x * TPB; base < ci.n_items; base += stride) {
-        const long long item = base + tc.tib;
+    for (long long it = 0; it < chunk; ++it) {
+        const long long item = first + it;
         const bool valid = item < ci.n_items;
-        const ItemRef ir = resolve_item(ci, valid ? item : base);
+        const ItemRef ir = cursor_item(ci, valid ? item : 0, cur);
         const cd* at = atilde + ir.problem * ci.at_stride;
         const cd* dg = diag + ir.problem * ci.dg_stride;
         int vbit[M];

@@ -196,12 +196,16 @@ __global__ void __launch_bounds__(kModpThreads) modp_term_kernel(
     const uint32_t p = M.p;
     const uint32_t inv2 = tab[2];
     unsigned long long my_sum = 0;  // lane 0: this team's terms (each < p)
-    const long long stride = (long long)gridDim.x * TPB;
+    // contiguous per-team runs of the class's items (Gosper's step, ItemCursor)
+    const long long n_teams = (long long)gridDim.x * TPB;
+    const long long chunk = (ci.n_items + n_teams - 1) / n_teams;
+    const long long first = ((long long)blockIdx.x * TPB + tc.tib) * chunk;
+    ItemCursor cur;
 
-    for (long long base = (long long)blockIdx.x * TPB; base < ci.n_items; base += stride) {
-        const long long item = base + tc.tib;
+    for (long long it = 0; it < chunk; ++it) {
+        const long long item = first + it;
         const bool valid = item < ci.n_items;
-        const ItemRef ir = resolve_item(ci, valid ? item : base);
+        const ItemRef ir = cursor_item(ci, valid ? item : 0, cur);
         int vbit[MH];
         {
             uint32_t mm = ir.mask;

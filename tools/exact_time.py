@@ -1,5 +1,8 @@
 """Time the exact GF(p) mode: cfg3 (n=40) and a 0/1 n=52 graph."""
+import sys
 import time
+
+sys.path.insert(0, ".")
 
 import numpy as np
 

@@ -264,7 +264,10 @@ __global__ void __launch_bounds__(kMirrorThreads) mirror_term_kernel(
                 // deferred row operation of my row on column i (applied at iteration myrow)
                 const cd xn = mnz ? m_sub(hri, m_mul(mu, pri)) : hri;
                 if (m_nz(mi)) {
-                    if (myrow == i) acc = m_sub(acc, m_mul(mu, P));  // row op, column j+1
+                    // row op on column j+1 (lane myrow == i): computed by every lane and
+                    // selected, so no divergent region (same IEEE result for that lane)
+                    const cd ra = m_sub(acc, m_mul(mu, P));
+                    if (myrow == i) acc = ra;
                     const cd v = (elim && myrow <= i) ? xn : hri;
                     acc = m_add(acc, m_mul(mi, v));                   // column op
                     P = m_add(P, m_mul(mi, pri));                     // pivot row's column op
@@ -315,7 +318,10 @@ __global__ void __launch_bounds__(kMirrorThreads) mirror_term_kernel(
                 }
                 for (int i = k - 1; i >= stop && i > 0; --i) {
                     const cd coef = CF[(k * (k - 1)) / 2 + i];
-                    if (m_nz(coef) && d < i) v = m_sub(v, m_mul(coef, PT[((i - 1) * i) / 2 + d]));
+                    // every lane computes, d < i selects (no divergent region; the read for
+                    // d >= i lands on a finite neighbouring table entry and is discarded)
+                    const cd t = m_sub(v, m_mul(coef, PT[((i - 1) * i) / 2 + d]));
+                    if (m_nz(coef) && d < i) v = t;
                 }
                 Pk[d] = v;
             }

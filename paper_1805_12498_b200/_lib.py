@@ -16,7 +16,8 @@ import numpy as np
 from .errors import DeviceError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhafb200.so")
+# HAFB200_LIB overrides the in-tree library (dev: A/B timing of build variants)
+LIB_PATH = os.environ.get("HAFB200_LIB") or os.path.join(_HERE, "libhafb200.so")
 ABI_VERSION = 1
 
 _lock = threading.Lock()

@@ -53,7 +53,8 @@ def _flags(verbose):
     f = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "-I", os.path.join(REPO, "include")] + ([f"-DHAFB_STAGGER={os.environ['HAFB_STAGGER']}"] if os.environ.get("HAFB_STAGGER") else []) \
         + ([f"-DHAFB_SMEM_HI={os.environ['HAFB_SMEM_HI']}"] if os.environ.get("HAFB_SMEM_HI") else []) \
-        + ([f"-DHAFB_REG_THREADS={os.environ['HAFB_REG_THREADS']}"] if os.environ.get("HAFB_REG_THREADS") else [])
+        + ([f"-DHAFB_REG_THREADS={os.environ['HAFB_REG_THREADS']}"] if os.environ.get("HAFB_REG_THREADS") else []) \
+        + (os.environ["HAFB_EXTRA_FLAGS"].split() if os.environ.get("HAFB_EXTRA_FLAGS") else [])
     if verbose:
         f.append("-Xptxas=-v")
     return f

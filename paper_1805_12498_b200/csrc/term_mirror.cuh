@@ -30,6 +30,14 @@
 namespace hafb {
 
 constexpr int kMirrorThreads = 64;
+#ifndef MIRROR_CP_UNROLL
+#define MIRROR_CP_UNROLL 4
+#endif
+#ifndef MIRROR_HS_UNROLL
+#define MIRROR_HS_UNROLL 1
+#endif
+constexpr int kMirrorCpUnroll = MIRROR_CP_UNROLL;  // charpoly i-loop unroll
+constexpr int kMirrorHsUnroll = MIRROR_HS_UNROLL;  // Hessenberg column-loop unroll
 
 // teams per block: one team per block from W = 32 up (the kernel is latency-bound and
 // shared-memory-limited, so single-team blocks let leftover shared memory host one
@@ -256,7 +264,7 @@ __global__ void __launch_bounds__(kMirrorThreads) mirror_term_kernel(
             if (elim) MU[myrow] = mu;
             tc.sync();
             const cd* prow = H + lp;  // the pivot row in place: h[j+1][i] = prow[i*LD]
-#pragma unroll 1
+#pragma unroll kMirrorHsUnroll
             for (int i = j + 2; i < S; ++i) {
                 const cd mi = MU[i];
                 const cd hri = lane < S ? H[i * LD + lane] : mk(0.0, 0.0);
@@ -316,6 +324,7 @@ __global__ void __launch_bounds__(kMirrorThreads) mirror_term_kernel(
                     const cd base0 = d >= 1 ? Pk1[d - 1] : mk(0.0, 0.0);
                     v = m_sub(base0, m_mul(hk, Pk1[d]));
                 }
+#pragma unroll kMirrorCpUnroll
                 for (int i = k - 1; i >= stop && i > 0; --i) {
                     const cd coef = CF[(k * (k - 1)) / 2 + i];
                     // every lane computes, d < i selects (no divergent region; the read for

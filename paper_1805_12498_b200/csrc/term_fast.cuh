@@ -1442,40 +1442,57 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
         cd* A = ws + L::A;
         int bad = 0;
         cd eD = mk(0.0, 0.0);
-        constexpr bool QS = !LOOPS && W == 32 && HAFB_QSERIES;
+        constexpr bool QS = !LOOPS && W <= 32 && HAFB_QSERIES;
         if constexpr (QS) {
             // Without loop weights the series is exp(sum_k t_k x^k / (2k)) = q(x)^(-1/2) with
             // q(x) = det(I - xB) = sum_j a_j x^j, a_j = A[S-j] (the reversed charpoly), so
             // Newton's identities and the exp recurrence (_numba.py:228-250, :276-294)
             // collapse into ONE recurrence from q g' = -(1/2) q' g:
             //   g_0 = 1,  g_k = -(1/k) sum_{j=1}^{min(k,S)} a_j (k - j/2) g_{k-j},
-            // evaluated in push form (lane k-1 accumulates g_k; each g_m is broadcast once).
-            // Exact in exact arithmetic; a non-finite coefficient or result -> status 2.
-            static_assert(R == 1, "one coefficient chunk per lane");
-            const int k = lane + 1;
-            cd acc = mk(0.0, 0.0);
+            // evaluated in push form (lane (k-1) % W, chunk (k-1) / W accumulates g_k; each g_m
+            // is broadcast once).  Exact in exact arithmetic; a non-finite coefficient or
+            // result -> status 2.
+            cd acc[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) acc[r] = mk(0.0, 0.0);
             const int src0 = ((int)(threadIdx.x & 31) & ~(W - 1));
             for (int m = 0; m < D; ++m) {
                 cd gm;
                 if (m == 0) {
                     gm = mk(1.0, 0.0);
                 } else {
+                    const int chunk = (m - 1) / W;
+                    cd v = acc[0];
+#pragma unroll
+                    for (int r = 1; r < R; ++r)
+                        if (r == chunk) v = acc[r];
                     const double sc = -INV[m];
-                    gm.re = __shfl_sync(tc.wmask, acc.re, src0 + m - 1) * sc;
-                    gm.im = __shfl_sync(tc.wmask, acc.im, src0 + m - 1) * sc;
+                    gm.re = __shfl_sync(tc.wmask, v.re, src0 + (m - 1) % W) * sc;
+                    gm.im = __shfl_sync(tc.wmask, v.im, src0 + (m - 1) % W) * sc;
                 }
-                const int j = k - m;
-                const bool on = k <= D && j >= 1 && j <= S;
-                // zero weight instead of a divergent region (the index is clamped in range)
-                const double wgt = on ? 0.5 * (double)(k + m) : 0.0;
-                acc = f_cma(acc, A[S - (on ? j : 1)], mk(wgt * gm.re, wgt * gm.im));
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int k = lane + 1 + W * r;
+                    const int j = k - m;
+                    const bool on = k <= D && j >= 1 && j <= S;
+                    // zero weight instead of a divergent region (the index is clamped in range)
+                    const double wgt = on ? 0.5 * (double)(k + m) : 0.0;
+                    acc[r] = f_cma(acc[r], A[S - (on ? j : 1)], mk(wgt * gm.re, wgt * gm.im));
+                }
             }
-            if (lane < S + 1) {
-                const cd a = A[lane];
+            for (int i = lane; i <= S; i += W) {
+                const cd a = A[i];
                 if (!isfinite(a.re) || !isfinite(a.im)) bad = 1;
             }
-            eD = mk(-acc.re * INV[D], -acc.im * INV[D]);
-            if (lane == D - 1 && (!isfinite(eD.re) || !isfinite(eD.im))) bad = 1;
+            {
+                const int chunk = (D - 1) / W;
+                cd v = acc[0];
+#pragma unroll
+                for (int r = 1; r < R; ++r)
+                    if (r == chunk) v = acc[r];
+                eD = mk(-v.re * INV[D], -v.im * INV[D]);
+            }
+            if (lane == (D - 1) % W && (!isfinite(eD.re) || !isfinite(eD.im))) bad = 1;
             bad = __any_sync(tc.wmask, bad);
         } else {
         {

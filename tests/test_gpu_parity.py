@@ -431,3 +431,27 @@ def test_fast_nsx_zero_columns_counting():
     assert abs(got - count) <= max(1e-10 * count, 1e-15 * abs_sum), (abs(got - count) / count)
     mirror = engine.hafnian(ac, backend="charpoly", arith="mirror")
     assert abs(got - count) <= abs(mirror - count)  # no worse than the reference here
+
+
+@pytest.mark.parametrize("n", [60, 62])
+def test_fast_terms_at_the_size_limit(n):
+    """n = 60, 62 (D up to kDMax = 31): FAST terms of sampled masks from every class
+    from S = 2 to S = n against the bit-exact oracle."""
+    rng = np.random.default_rng(n)
+    g = rng.normal(0, np.sqrt(0.5), (n, n)) + 1j * rng.normal(0, np.sqrt(0.5), (n, n))
+    a = (g + g.T) / 2 / np.sqrt(n)
+    at, dg, nh = engine._prepare(a, False)
+    masks = []
+    for m in range(1, nh + 1):
+        for _ in range(3):
+            bits = rng.choice(nh, size=m, replace=False)
+            masks.append(int(sum(1 << int(b) for b in bits)))
+    masks = np.array(masks, dtype=np.uint64)
+    ref, rst = O.terms(at, dg, nh, masks, backend=1)
+    got, st = kernels.terms(at, dg, nh, masks, 1, False, arith="fast")
+    assert np.array_equal(st, rst)
+    pc = np.array([bin(int(x)).count("1") for x in masks])
+    for m in range(1, nh + 1):
+        sel = pc == m
+        scale = np.abs(ref[sel]).max()
+        assert np.abs(got[sel] - ref[sel]).max() <= 1e-9 * scale, (m, np.abs(got[sel] - ref[sel]).max() / scale)

@@ -91,14 +91,6 @@ constexpr int kDMax = 31;
 #ifndef NS_HIKEY
 #define NS_HIKEY 1
 #endif
-#ifndef NS_PAIR
-#define NS_PAIR 0
-#endif
-// threshold pivoting for the static-column kernel (100 = classic partial pivoting;
-// 50 measured 3 % slower at S = 28: the extra ballot/shuffle outweighs skipped swaps)
-#ifndef NS_TAU_PCT
-#define NS_TAU_PCT 100
-#endif
 #ifndef NS_BRANCHLESS
 #define NS_BRANCHLESS 1
 #endif
@@ -107,9 +99,6 @@ constexpr int kDMax = 31;
 #endif
 #ifndef HAFB_QSERIES
 #define HAFB_QSERIES 1
-#endif
-#ifndef HAFB_CPRE
-#define HAFB_CPRE 0
 #endif
 #ifndef HAFB_NS_HI
 #define HAFB_NS_HI 32
@@ -637,19 +626,6 @@ __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const Team
 #endif
         unsigned mx = __reduce_max_sync(tm, (kb & ~63u) | (unsigned)(63 - lane));
         int wl = 63 - (int)(mx & 63u);
-#if NS_TAU_PCT < 100
-        if constexpr (W <= 32) {
-            // threshold partial pivoting: keep the natural pivot row J+1 when its entry is
-            // within NS_TAU of the column maximum (multipliers stay below 1/NS_TAU): no swap
-            const unsigned nb = __ballot_sync(tm, myrow == J + 1) >> tb;
-            const int nl = nb ? __ffs(nb) - 1 : 0;
-            const double nk = __shfl_sync(tm, key, tb + nl);
-            if (nb && nk > 0.0 && nk * 100.0 >= (double)NS_TAU_PCT * __hiloint2double((int)(mx & ~63u), 0)) {
-                wl = nl;
-                mx = (mx & ~63u) | (unsigned)(63 - nl);
-            }
-        }
-#endif
 #if NS_SPECINV
         cd ip;
 #endif
@@ -750,33 +726,6 @@ __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const Team
         // sweep, columns S-1 down to J+2: row update fused with the column gemv; at J+2
         // stash the next step's column J+2 and finish column J+1 (the gemv target)
         cd acc0 = mk(0.0, 0.0), acc1 = mk(0.0, 0.0);
-#if NS_PAIR
-        // columns in pairs (c, c-1) under one exit test: the pair that holds J+2 may also
-        // hold J+1, whose register copy is dead (it travels in hn) and whose multiplier is
-        // zero, so updating it is harmless
-        cd pa = pr[S - 1], ma = mus[S - 1], pb = pr[S - 2], mb = mus[S - 2];
-        static_for<0, S - 2, 2>([&](auto ii) {
-            constexpr int c = S - 1 - decltype(ii)::value;
-            const cd pn = pr[c - 2], mn = mus[c - 2];  // next pair's broadcasts
-            const cd pm = pr[c >= 3 ? c - 3 : 0], mm = mus[c >= 3 ? c - 3 : 0];
-            w[c] = f_cms(w[c], mu, pa);
-            w[c - 1] = f_cms(w[c - 1], mu, pb);
-            acc1 = f_cma(acc1, ma, w[c]);
-            acc0 = f_cma(acc0, mb, w[c - 1]);
-            if (c - 1 <= J + 2) {
-                const cd nh = c == J + 2 ? w[c] : w[c - 1];
-                const cd p1 = pr[J + 1];
-                hj = f_add(f_cms(hn, mu, p1), f_add(acc0, acc1));
-                hn = nh;
-                return false;
-            }
-            pa = pn;
-            ma = mn;
-            pb = pm;
-            mb = mm;
-            return true;
-        });
-#else
         cd pa = pr[S - 1], ma = mus[S - 1];
         static_for<0, S - 2>([&](auto ii) {
             constexpr int c = S - 1 - decltype(ii)::value;
@@ -794,7 +743,6 @@ __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const Team
             }
             return true;
         });
-#endif
         HT_MARK(11);
     }
     // logical columns S-2 (hj) and S-1 (hn): every row
@@ -1299,54 +1247,6 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
             cd prodl = mk(1.0, 0.0);
             cd prodx = mk(1.0, 0.0);
             cd Q[NSX ? S - 32 : 1] = {};  // extra coefficients (NSX)
-            if constexpr (!SH && W <= 32 && HAFB_CPRE) {
-                // The recurrence's coefficients cf(k, l) = h(l, k-1) prod_{j=l+1}^{k-1} h(j, j-1)
-                // do not depend on the polynomials: lane l forms them all up front (its running
-                // subdiagonal product, same operation order as the per-step form below) and
-                // stores them IN PLACE over h(l, k-1) -- the diagonal and the subdiagonal the
-                // recurrence still reads are never overwritten.  The recurrence then runs
-                // without a barrier per step and the compiler overlaps consecutive steps.
-                cd* Hm = ws + L::HS;
-                cd prod = mk(1.0, 0.0);
-                // branch-free: every lane runs every column (lanes >= c compute and drop)
-                const int lsafe = lane < S ? lane : 0;
-                static_for<1, S>([&](auto cc) {
-                    constexpr int c = decltype(cc)::value;
-                    const cd beta = Hm[((c - 1) * (c + 2)) / 2 + c];  // h[c][c-1]
-                    const cd np = f_mul(lane == c - 1 ? mk(1.0, 0.0) : prod, beta);
-                    const bool on = lane < c;
-                    prod = on ? np : prod;
-                    cd* e = Hm + (c * (c + 3)) / 2 + (on ? lane : lsafe);
-                    const cd v = f_mul(*e, prod);
-                    if (on) *e = v;
-                    return true;
-                });
-                tc.sync();
-                static_for<1, S + 1>([&](auto kk) {
-                    constexpr int k = decltype(kk)::value;
-                    const cd* cfk = Hm + ((k - 1) * (k + 2)) / 2;  // cf(k, l) at l, h(k-1,k-1) at k-1
-                    cd prev;
-                    prev.re = tshfl_up<W>(P[k - 1].re, 1);
-                    prev.im = tshfl_up<W>(P[k - 1].im, 1);
-                    if (lane == 0) prev = mk(0.0, 0.0);
-                    // older terms (P_l, l <= k-2) in accumulators independent of P_{k-1}:
-                    // without a per-step barrier they overlap the previous step's chain
-                    cd acc1 = mk(0.0, 0.0), acc2 = mk(0.0, 0.0), acc3 = mk(0.0, 0.0), acc4 = mk(0.0, 0.0);
-                    static_for<1, k>([&](auto jj) {
-                        constexpr int i = decltype(jj)::value;
-                        if constexpr ((i & 3) == 0) acc1 = f_cms(acc1, cfk[i - 1], P[i - 1]);
-                        else if constexpr ((i & 3) == 1) acc2 = f_cms(acc2, cfk[i - 1], P[i - 1]);
-                        else if constexpr ((i & 3) == 2) acc3 = f_cms(acc3, cfk[i - 1], P[i - 1]);
-                        else acc4 = f_cms(acc4, cfk[i - 1], P[i - 1]);
-                        return true;
-                    });
-                    cd acc = f_cms(prev, cfk[k - 1], P[k - 1]);
-                    acc = f_add(acc, f_add(f_add(acc1, acc2), f_add(acc3, acc4)));
-                    if constexpr (k < S) P[k] = acc;
-                    else if (lane < S) A[lane] = acc;
-                    return true;
-                });
-            } else
             static_for<1, S + 1>([&](auto kk) {
                 constexpr int k = decltype(kk)::value;
                 cd* cf = ws + L::CF + (k & 1) * S;

@@ -58,13 +58,18 @@ struct MirrorLayout {
     static constexpr int CF = 0;                         // coef_{k,i}: row k at k(k-1)/2 (S(S+1)/2)
     static constexpr int P = S * (S + 1) / 2;            // P_k: row k at k(k+1)/2, length k+1
     static constexpr int HS = AREA;                      // packed upper Hessenberg: column c at c(c+3)/2
-    static constexpr int MU = HS + (S - 1) * (S + 2) / 2 + S;  // [S+2] multipliers by logical row
-    static constexpr int T = MU + S + 2;                 // [kDMax+2] traces
+    static constexpr int HSN = (S - 1) * (S + 2) / 2 + S;
+    // the series scratch (T, SS, E: live after the charpoly) and the loop-chain vector (U:
+    // live before the reduction) share the packed Hessenberg's region, which is live only
+    // between the two (shared memory limits this kernel's teams per SM)
+    static constexpr bool ALIAS = HSN >= 3 * (kDMax + 2) && HSN >= 2 * S;
+    static constexpr int T = ALIAS ? HS : HS + HSN;      // [kDMax+2] traces
     static constexpr int SS = T + kDMax + 2;             // [kDMax+2] series
     static constexpr int E = SS + kDMax + 2;             // [kDMax+2] exp Horner state
-    static constexpr int ELL = E + kDMax + 2;            // [kDMax+2] loop corrections
-    static constexpr int U = ELL + kDMax + 2;            // [2][S] loop-chain vector
-    static constexpr int RED = U + 2 * S;                // [8] cross-warp exchange (W = 64)
+    static constexpr int U = ALIAS ? HS : E + kDMax + 2;  // [2][S] loop-chain vector
+    static constexpr int MU = ALIAS ? HS + HSN : U + 2 * S;  // [S+2] multipliers by logical row
+    static constexpr int ELL = MU + S + 2;               // [kDMax+2] loop corrections
+    static constexpr int RED = ELL + kDMax + 2;          // [8] cross-warp exchange (W = 64)
     static constexpr int INTS = RED + 8;                 // int area (in cd slots)
     static constexpr int LMN = (2 * S + 3 * (S + 2) + 3) / 4 + 1;  // lm[2][S], stop[S+2], misc
     static constexpr int TOTAL = INTS + LMN;

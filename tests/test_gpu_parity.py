@@ -455,3 +455,29 @@ def test_fast_terms_at_the_size_limit(n):
         sel = pc == m
         scale = np.abs(ref[sel]).max()
         assert np.abs(got[sel] - ref[sel]).max() <= 1e-9 * scale, (m, np.abs(got[sel] - ref[sel]).max() / scale)
+
+
+def test_fast_loop_terms_every_class_n40():
+    """Loop-hafnian FAST terms (loop chain + Newton/exp path; static-column kernel up to
+    S = 32, shared-memory kernel from S = 34) of sampled masks from every class of an
+    n = 40 problem against the bit-exact oracle."""
+    n = 40
+    rng = np.random.default_rng(40)
+    g = rng.normal(0, np.sqrt(0.5), (n, n)) + 1j * rng.normal(0, np.sqrt(0.5), (n, n))
+    a = (g + g.T) / 2 / np.sqrt(n)
+    np.fill_diagonal(a, rng.normal(0, np.sqrt(0.5), n) + 1j * rng.normal(0, np.sqrt(0.5), n))
+    at, dg, nh = engine._prepare(a, True)
+    masks = []
+    for m in range(1, nh + 1):
+        for _ in range(6):
+            bits = rng.choice(nh, size=m, replace=False)
+            masks.append(int(sum(1 << int(b) for b in bits)))
+    masks = np.array(masks, dtype=np.uint64)
+    ref, rst = O.terms(at, dg, nh, masks, backend=1, include_loops=True)
+    got, st = kernels.terms(at, dg, nh, masks, 1, True, arith="fast")
+    assert np.array_equal(st, rst)
+    pc = np.array([bin(int(x)).count("1") for x in masks])
+    for m in range(1, nh + 1):
+        sel = pc == m
+        scale = np.abs(ref[sel]).max()
+        assert np.abs(got[sel] - ref[sel]).max() <= 1e-9 * scale, (m, np.abs(got[sel] - ref[sel]).max() / scale)

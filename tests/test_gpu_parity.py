@@ -481,3 +481,26 @@ def test_fast_loop_terms_every_class_n40():
         sel = pc == m
         scale = np.abs(ref[sel]).max()
         assert np.abs(got[sel] - ref[sel]).max() <= 1e-9 * scale, (m, np.abs(got[sel] - ref[sel]).max() / scale)
+
+
+def test_fast_sharded_range_lists_reassemble_bit_exact_n36():
+    """FAST range partials over LPT shards (many segments per launch: each team's contiguous
+    mask walk crosses segment edges) equal the full run bit for bit at n = 36 (NSX, both
+    static-column team widths, staged gathers)."""
+    from paper_1805_12498_b200 import costmodel
+
+    rng = np.random.default_rng(36)
+    n = 36
+    g = rng.normal(0, np.sqrt(0.5), (n, n)) + 1j * rng.normal(0, np.sqrt(0.5), (n, n))
+    a = (g + g.T) / 2 / np.sqrt(n)
+    at, dg, nh = engine._prepare(a, False)
+    full, ff = kernels.sum_subsets_det(at, dg, nh, 1, False, 1, 512, arith="fast")
+    assert not ff.any()
+    for k in (3, 8):
+        shards = costmodel.lpt_shards(costmodel.range_costs(nh, 512), k)
+        got = np.zeros(512, np.complex128)
+        for sh in shards:
+            s, f = kernels.sum_range_list(at, dg, nh, 512, sh, 1, False, arith="fast")
+            assert not f.any()
+            got[sh] = s
+        assert (bits(got) == bits(full)).all()

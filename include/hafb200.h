@@ -155,6 +155,11 @@ int hafb_modp_sums(const uint32_t* atilde_p, const uint32_t* diag_p, const uint3
  * kernel (the roofline denominator for the subset-term kernels).  tflops = 2 flop/DFMA. */
 int hafb_fp64_peak(int device, double* tflops, double* ms);
 
+/* Release the library's cached device memory on `device` (its private stream-ordered
+ * pool keeps up to 8 GiB of freed buffers between calls; a large call such as n = 62
+ * can leave more until the next synchronisation). */
+int hafb_trim_pool(int device);
+
 /* Kernel launches issued by the calling thread since the last reset (the bench's
  * gpu_launches claim). */
 int64_t hafb_launch_count(int reset);

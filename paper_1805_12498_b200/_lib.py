@@ -54,6 +54,7 @@ SIGNATURES = {
     "hafb_sum_range_list_async": (_int, [_vp, _vp, _int, _int, _i32p, _int, _int, _int, _int,
                                          _int, _vp, _size, _vp, _vp, _vp, _vp]),
     "hafb_launch_count": (_i64, [_int]),
+    "hafb_trim_pool": (_int, [_int]),
     "hafb_fp64_peak": (_int, [_int, _dp, _dp]),
     "hafb_batch_raw": (_int, [_dp, _int, _int, _int, _int, _int, _int, _int, _int, ctypes.c_double,
                               _dp, _i64p, _i64p, _dp, _dp]),

@@ -20,8 +20,11 @@ from concurrent.futures import ThreadPoolExecutor
 PKG = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(os.environ.get("HAFB200_BUILD_DIR", "/tmp/hafb200_build"))
-LIB = os.path.join(PKG, "libhafb200.so")
+# objects live under the repo (git-ignored build/), one directory per flag set, so two
+# checkouts or two flag variants never overwrite each other's objects
+BUILD_ROOT = os.environ.get("HAFB200_BUILD_DIR", os.path.join(REPO, "build"))
+# HAFB200_LIB sends a variant build elsewhere (the in-tree library stays the default build)
+LIB = os.environ.get("HAFB200_LIB") or os.path.join(PKG, "libhafb200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FAST_SIZES = list(range(2, 49, 2))  # kFastSMax = 48 (csrc/fast_launch.h)
 MIRROR_SIZES = list(range(2, 63, 2))  # n <= 62
@@ -42,8 +45,19 @@ def _deps():
     return out
 
 
-def up_to_date() -> bool:
+def _stamp(flags) -> str:
+    """Identity of a build: the compile flags (environment-selected variants included)."""
+    import hashlib
+
+    return hashlib.sha256(" ".join(flags).encode()).hexdigest()[:16]
+
+
+def up_to_date(flags=None) -> bool:
     if not os.path.exists(LIB):
+        return False
+    stamp_path = LIB + ".stamp"
+    want = _stamp(flags if flags is not None else _flags(False))
+    if not os.path.exists(stamp_path) or open(stamp_path).read().strip() != want:
         return False
     t = os.path.getmtime(LIB)
     return all(os.path.getmtime(d) <= t for d in _deps())
@@ -72,11 +86,13 @@ def _units():
 
 
 def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -> str:
-    if not force and up_to_date():
+    flags = _flags(verbose)
+    stamp_flags = [f for f in flags if f != "-Xptxas=-v"]
+    if not force and up_to_date(stamp_flags):
         return LIB
+    OBJ = os.path.join(BUILD_ROOT, "obj-" + _stamp(stamp_flags))
     os.makedirs(OBJ, exist_ok=True)
     cc = nvcc()
-    flags = _flags(verbose)
 
     def compile_one(u):
         obj, src, extra = u
@@ -99,6 +115,8 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
     objs = [os.path.join(OBJ, u[0]) for u in _units()]
     subprocess.run([cc, *ARCH, "--shared", "-o", LIB + ".tmp", *objs], check=True)
     os.replace(LIB + ".tmp", LIB)
+    with open(LIB + ".stamp", "w") as f:
+        f.write(_stamp(stamp_flags) + "\n")
     return LIB
 
 

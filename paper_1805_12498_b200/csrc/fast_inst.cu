@@ -71,7 +71,9 @@ static cudaError_t launch_one(const cd* at, const cd* dg, int n_half, const Clas
     const int stage = (NT > kFastThreads && !SH && base_smem + a_bytes <= (size_t)optin) ? 1 : 0;
     const size_t smem = base_smem + (stage ? a_bytes : 0);
     auto kern = fast_term_kernel<S, L, SH, NT>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // smem depends on n (the staged Atilde): the attribute is the size-independent
+    // opt-in maximum, so host threads launching different n never race on it
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
     if (e != cudaSuccess) return e;
     int occ = 1;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);

@@ -51,6 +51,36 @@ int check_common(int n_half, int backend, int arith) {
     return HAFB_OK;
 }
 
+// The library's own stream-ordered memory pool per device (the process's default
+// pool is left alone).  Freed buffers stay in it up to kPoolKeepBytes, so repeated
+// calls up to n = 56 reuse their term buffers without driver allocations; beyond
+// that the excess returns to the driver at the next synchronisation, and
+// hafb_trim_pool() releases everything (e.g. after an n = 62 call).
+constexpr unsigned long long kPoolKeepBytes = 8ull << 30;
+
+cudaError_t library_pool(int device, cudaMemPool_t* out) {
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
+    if (device < 0 || device >= 64) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> g(mu);
+    if (!pools[device]) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = device;
+        cudaMemPool_t p;
+        cudaError_t e = cudaMemPoolCreate(&p, &props);
+        if (e != cudaSuccess) return e;
+        unsigned long long thr = kPoolKeepBytes;
+        e = cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr);
+        if (e != cudaSuccess) return e;
+        pools[device] = p;
+    }
+    *out = pools[device];
+    return cudaSuccess;
+}
+
 // One host call: its own non-blocking stream and stream-ordered allocations,
 // released (after a stream sync) when the call returns on any path.
 struct Call {
@@ -59,29 +89,15 @@ struct Call {
     cudaError_t open(int device) {
         cudaError_t e = cudaSetDevice(device);
         if (e != cudaSuccess) return e;
-        e = keep_pool(device);
+        e = library_pool(device, &pool);
         if (e != cudaSuccess) return e;
         return cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
     }
-    // keep freed stream-ordered memory in the device pool across calls (the default
-    // release threshold of 0 hands it back to the driver at every synchronisation)
-    static cudaError_t keep_pool(int device) {
-        static std::once_flag once[64];
-        cudaError_t err = cudaSuccess;
-        if (device < 0 || device >= 64) return cudaErrorInvalidDevice;
-        std::call_once(once[device], [&] {
-            cudaMemPool_t pool;
-            err = cudaDeviceGetDefaultMemPool(&pool, device);
-            if (err != cudaSuccess) return;
-            unsigned long long thr = ~0ull;
-            err = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        });
-        return err;
-    }
+    cudaMemPool_t pool = nullptr;
     template <class T>
     cudaError_t alloc(T** p, size_t bytes) {
         void* q = nullptr;
-        cudaError_t e = cudaMallocAsync(&q, std::max<size_t>(bytes, 16), st);
+        cudaError_t e = cudaMallocFromPoolAsync(&q, std::max<size_t>(bytes, 16), pool, st);
         if (e == cudaSuccess) bufs.push_back(q);
         *p = static_cast<T*>(q);
         return e;
@@ -534,6 +550,15 @@ int hafb_device_count(void) {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
     return n;
+}
+
+int hafb_trim_pool(int device) {
+    cudaMemPool_t pool;
+    CK(library_pool(device, &pool));
+    CK(cudaSetDevice(device));
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemPoolTrimTo(pool, 0));
+    return HAFB_OK;
 }
 
 int64_t hafb_launch_count(int reset) {

@@ -1085,8 +1085,9 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
     cd* As = reinterpret_cast<cd*>(INV + kDMax + 1);
     const int ldA = n + 1;
     long long staged_problem = -1;
-    if (stage_a) {
-        staged_problem = ((long long)blockIdx.x * TPB * chunk) / ci.per_problem;
+    const long long block_first = (long long)blockIdx.x * TPB * chunk;
+    if (stage_a && block_first < ci.n_items) {  // a block past the last item stages nothing
+        staged_problem = block_first / ci.per_problem;
         const cd* src = atilde + staged_problem * ci.at_stride;
         for (int i = threadIdx.x; i < n * n; i += blockDim.x) As[(i / n) * ldA + (i % n)] = src[i];
     }

@@ -42,6 +42,11 @@ def _arith_id(arith) -> int:
     return ARITH_MODES[a]
 
 
+def device_count() -> int:
+    """Visible CUDA devices (0 without a GPU; the library must still load)."""
+    return int(_lib.load(require_device=False).hafb_device_count())
+
+
 def _device(device) -> int:
     return int(os.environ.get("HAFB200_DEVICE", "0")) if device is None else int(device)
 

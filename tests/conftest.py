@@ -46,6 +46,16 @@ def bits(a):
     return np.ascontiguousarray(a, dtype=np.complex128).view(np.uint64)
 
 
+def digest(A) -> int:
+    """8-byte fingerprint of a matrix's exact bits.  cfg1 inputs go through LAPACK QR,
+    which may differ in the last ulp on another CPU: tests regenerate the batch and
+    compare digests with the fixture's before demanding bit-identity."""
+    import hashlib
+
+    h = hashlib.blake2b(np.ascontiguousarray(A, np.complex128).tobytes(), digest_size=8)
+    return int.from_bytes(h.digest(), "little")
+
+
 def load_golden(name):
     path = os.path.join(GOLDEN, name)
     if not os.path.exists(path):

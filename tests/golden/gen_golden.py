@@ -44,6 +44,9 @@ from hafnium.kernels import _numba as nb  # noqa: E402
 
 from paper_1805_12498_b200 import workloads as W  # noqa: E402
 
+sys.path.insert(0, os.path.dirname(HERE))
+from conftest import digest  # noqa: E402
+
 THREADS = os.cpu_count()
 
 
@@ -188,6 +191,21 @@ def gen_range_n52():
     np.savez_compressed(os.path.join(HERE, "range_n52.npz"), **out)
 
 
+def gen_batch(count: int = 4096):
+    """cfg1: the full 4096-matrix batch through the reference's public API, looped as
+    the reference itself has to (no batch API; SURVEY.md finding 6), both backends."""
+    out = {"seeds": np.arange(count, dtype=np.int64)}
+    mats = [W.cfg1(s) for s in range(count)]
+    out["digests"] = np.array([digest(a) for a in mats], dtype=np.uint64)
+    for backend, bname in ((1, "charpoly"), (0, "spectral")):
+        t0 = time.time()
+        res = np.array([hafnium.hafnian(a, backend=bname, threads=THREADS) for a in mats])
+        out[f"result_b{backend}"] = res
+        out[f"seconds_b{backend}"] = np.array(time.time() - t0)
+        print(f"batch cfg1 x{count} {bname}: {time.time() - t0:.1f}s", flush=True)
+    np.savez_compressed(os.path.join(HERE, "batch_cfg1.npz"), **out)
+
+
 def gen_powertraces():
     out = {}
     rng = np.random.default_rng(2024)
@@ -223,3 +241,5 @@ if __name__ == "__main__":
         gen_ranges()
     if "range_n52" in which:
         gen_range_n52()
+    if "batch" in which:
+        gen_batch()

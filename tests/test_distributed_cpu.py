@@ -70,3 +70,57 @@ def test_sharded_gather_bit_identical(world, n, loops):
     for rank, res, fails in out:
         assert fails == 0
         assert res == ref, (rank, res, ref)
+
+
+def _bench_worker(rank, world, port, q):
+    """bench.py's N>1 step orchestration with the device call mocked by the oracle: the
+    rank's LPT shard of the fixed ranges -> its partials in a padded complex tensor ->
+    bench.gather_shards (the all-gather) -> bench.assemble (range order + fixed tree);
+    bench.max_over_ranks for the timing."""
+    import torch
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    from oracle import oracle as O
+    from paper_1805_12498_b200 import costmodel, workloads
+    from paper_1805_12498_b200.engine import _prepare
+
+    A = workloads.cfg0(n=18)
+    at, dg, nh = _prepare(A, False)
+    nr = min((1 << nh) - 1, bench.N_RANGES)
+    shards = costmodel.lpt_shards(costmodel.range_costs(nh, nr), world)
+    width = max(len(s) for s in shards)
+    bounds = costmodel.range_bounds(nh, nr)
+    local = torch.zeros(width, dtype=torch.complex128)
+    for i, r in enumerate(shards[rank]):  # the mocked device call
+        ps, _ = O.sum_mask_range(at, dg, nh, *bounds[r], 1, backend=1, threads=1)
+        local[i] = complex(ps[0])
+    gathered = [torch.zeros(width, dtype=torch.complex128) for _ in shards]
+    bench.gather_shards(local, gathered, dist)
+    res = bench.assemble(shards, gathered)
+    t = bench.max_over_ranks([0.5 + rank, 3.0 - rank], dist, torch.device("cpu"))
+    q.put((rank, res, t))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_bench_multirank_orchestration_gloo():
+    from oracle import oracle as O
+    from paper_1805_12498_b200 import workloads
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    ref, _ = O.hafnian(workloads.cfg0(n=18), 1)
+    for rank, res, t in out:
+        assert res == ref, (rank, res, ref)
+        assert t == [1.5, 3.0]

@@ -65,18 +65,14 @@ static cudaError_t launch_one(const cd* at, const cd* dg, int n_half, const Clas
     // the one-block-per-SM register classes stage Atilde in shared memory when it fits
     const int n = 2 * n_half;
     const size_t a_bytes = (size_t)n * (n + 1) * sizeof(cd);
-    int optin = 0, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const int optin = device_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin);
     const int stage = (NT > kFastThreads && !SH && base_smem + a_bytes <= (size_t)optin) ? 1 : 0;
     const size_t smem = base_smem + (stage ? a_bytes : 0);
     auto kern = fast_term_kernel<S, L, SH, NT>;
     // smem depends on n (the staged Atilde): the attribute is the size-independent
     // opt-in maximum, so host threads launching different n never race on it
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-    if (e != cudaSuccess) return e;
     int occ = 1;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);
+    cudaError_t e = launch_config((const void*)kern, NT, smem, optin, &occ);
     if (e != cudaSuccess) return e;
     const long long want = (ci.n_items + TPB - 1) / TPB;
     const long long cap_blocks = (long long)sms * std::max(occ, 1);

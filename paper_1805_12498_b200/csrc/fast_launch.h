@@ -5,10 +5,70 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+#include <utility>
+#include <vector>
+
 #include "cplx.cuh"
 #include "enumerate.cuh"
 
 namespace hafb {
+
+// Per-(kernel, device, block size, smem) launch configuration, computed once: the max
+// dynamic shared memory attribute (set to `smem_attr`, a size-independent value, so
+// concurrent host threads never race on it) and the occupancy.  The two runtime
+// queries cost tens of microseconds per launch, which dominated small problems (a
+// hafnian of n = 20 is ~12 launches of a few microseconds each).
+inline cudaError_t launch_config(const void* kern, int threads, size_t smem, int smem_attr,
+                                 int* occ) {
+    struct Entry {
+        const void* k;
+        int dev, threads;
+        size_t smem;
+        int occ;
+    };
+    static std::mutex mu;
+    static std::vector<Entry> cache;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    {
+        std::lock_guard<std::mutex> g(mu);
+        for (const Entry& x : cache)
+            if (x.k == kern && x.dev == dev && x.threads == threads && x.smem == smem) {
+                *occ = x.occ;
+                return cudaSuccess;
+            }
+    }
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_attr);
+    if (e != cudaSuccess) return e;
+    int o = 1;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, smem);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> g(mu);
+    cache.push_back(Entry{kern, dev, threads, smem, o});
+    *occ = o;
+    return cudaSuccess;
+}
+
+// Device attributes, cached per device.
+inline int device_attr(cudaDeviceAttr a) {
+    static std::mutex mu;
+    static std::vector<std::pair<long long, int>> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const long long key = (long long)dev * 1000 + (long long)a;
+    {
+        std::lock_guard<std::mutex> g(mu);
+        for (auto& x : cache)
+            if (x.first == key) return x.second;
+    }
+    int v = 0;
+    cudaDeviceGetAttribute(&v, a, dev);
+    std::lock_guard<std::mutex> g(mu);
+    cache.emplace_back(key, v);
+    return v;
+}
 
 constexpr int kFastSMax = 48;  // sizes above run in the shared-memory kernel
 

@@ -113,19 +113,9 @@ struct Call {
 // Kernels whose dynamic shared memory varies per launch get the opt-in maximum as
 // their attribute (a per-launch value would race between host threads launching
 // the same kernel with different sizes).
-int smem_optin() {
-    int dev = 0, v = 227 * 1024;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    return v;
-}
+int smem_optin() { return device_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin); }
 
-int sm_count() {
-    int dev = 0, v = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-}
+int sm_count() { return device_attr(cudaDevAttrMultiProcessorCount); }
 
 template <int B, bool L>
 cudaError_t launch_terms_t(const cd* at, const cd* dg, int n_half, MaskMap map, long long per,
@@ -136,10 +126,8 @@ cudaError_t launch_terms_t(const cd* at, const cd* dg, int n_half, MaskMap map, 
     int wpb = (int)std::min<size_t>(8, std::max<size_t>(1, (200 * 1024) / per_warp));
     size_t smem = wpb * per_warp;
     auto kern = terms_smem_kernel<B, L>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin());
-    if (e != cudaSuccess) return e;
     int occ = 1;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, wpb * 32, smem);
+    cudaError_t e = launch_config((const void*)kern, wpb * 32, smem, smem_optin(), &occ);
     if (e != cudaSuccess) return e;
     long long want = (total + wpb - 1) / wpb;
     long long cap_blocks = (long long)sm_count() * std::max(occ, 1);
@@ -253,10 +241,8 @@ cudaError_t launch_smem_class(const cd* at, const cd* dg, int n_half, const Clas
     int wpb = (int)std::min<size_t>(8, std::max<size_t>(1, (200 * 1024) / per_warp));
     size_t smem = wpb * per_warp;
     auto kern = terms_smem_class_kernel<B, L>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin());
-    if (e != cudaSuccess) return e;
     int occ = 1;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, wpb * 32, smem);
+    cudaError_t e = launch_config((const void*)kern, wpb * 32, smem, smem_optin(), &occ);
     if (e != cudaSuccess) return e;
     long long want = (ci.n_items + wpb - 1) / wpb;
     int grid = (int)std::max<long long>(1, std::min(want, (long long)sm_count() * std::max(occ, 1)));
@@ -353,12 +339,19 @@ int upload_tables(int D, const std::vector<Seg>& segs, void* table_ws, cudaStrea
     dt.prefix = reinterpret_cast<long long*>(p);
     p += align256(sizeof(long long) * dt.t.prefix.size());
     dt.base = reinterpret_cast<unsigned long long*>(p);
-    CK(cudaMemcpyAsync(dt.binom, g_binom_host, sizeof(g_binom_host), cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(dt.segs, segs.data(), sizeof(Seg) * nseg, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(dt.prefix, dt.t.prefix.data(), sizeof(long long) * dt.t.prefix.size(),
-                       cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(dt.base, dt.t.base.data(), sizeof(unsigned long long) * dt.t.base.size(),
-                       cudaMemcpyHostToDevice, st));
+    // one host staging image of the four tables, one copy (a pageable copy costs
+    // ~10 us each; small problems are launch- and copy-bound)
+    const size_t total = (size_t)(reinterpret_cast<char*>(dt.base) - static_cast<char*>(table_ws)) +
+                         sizeof(unsigned long long) * dt.t.base.size();
+    std::vector<char> img(total);
+    char* h = img.data();
+    auto at_ = [&](const void* dptr) { return h + (static_cast<const char*>(dptr) - static_cast<char*>(table_ws)); };
+    std::memcpy(at_(dt.binom), g_binom_host, sizeof(g_binom_host));
+    std::memcpy(at_(dt.segs), segs.data(), sizeof(Seg) * nseg);
+    std::memcpy(at_(dt.prefix), dt.t.prefix.data(), sizeof(long long) * dt.t.prefix.size());
+    std::memcpy(at_(dt.base), dt.t.base.data(), sizeof(unsigned long long) * dt.t.base.size());
+    // pageable source: the runtime stages it before returning, so `img` may go away
+    CK(cudaMemcpyAsync(table_ws, img.data(), total, cudaMemcpyHostToDevice, st));
     return HAFB_OK;
 }
 
@@ -497,7 +490,7 @@ int enqueue_range_list(const cd* at, const cd* dg, int n_half, int n_ranges, con
 
 // single-warp kernels for the power-trace entry points
 __global__ void power_traces_kernel(const cd* b, int m, int K, int backend, int cap_mult,
-                                    cd* traces, int* ok, cd* ws) {
+                                    cd* traces, int* ok, long long* sweeps, cd* ws) {
     int lane = threadIdx.x & 31;
     WarpWs w = carve(ws, m + (m & 1));
     for (int e = lane; e < m * m; e += 32) w.H[e] = b[e];
@@ -510,9 +503,11 @@ __global__ void power_traces_kernel(const cd* b, int m, int K, int backend, int 
             *ok = traces_from_charpoly_seq(a, m, K, traces) ? 1 : 0;
         }
     } else {
-        bool conv = hess_eigvals_smem(w.H, m, cap_mult, w.eig, lane);
+        long long nsw = 0;
+        bool conv = hess_eigvals_smem(w.H, m, cap_mult, w.eig, lane, &nsw);
         __syncwarp();
         if (lane == 0) {
+            *sweeps = nsw;  // QR sweeps, as _numba.power_traces_spectral returns (:415-422)
             // _power_sums (_numba.py:191-200)
             for (int k = 0; k < K; ++k) traces[k] = mk(0.0, 0.0);
             for (int i = 0; i < m; ++i) {
@@ -1004,20 +999,25 @@ int hafb_power_traces(const double* b, int m, int K, int backend, int cap_mult, 
     Call c;
     cd *d_b, *d_t, *d_ws;
     int* d_ok;
+    long long* d_sw;
     int h_ok = 0;
+    long long h_sw = 0;
     CK(c.open(device));
     CK(c.alloc(&d_b, sizeof(cd) * m * m));
     CK(c.alloc(&d_t, sizeof(cd) * K));
     CK(c.alloc(&d_ok, sizeof(int)));
+    CK(c.alloc(&d_sw, sizeof(long long)));
+    CK(cudaMemsetAsync(d_sw, 0, sizeof(long long), c.st));
     CK(c.alloc(&d_ws, sizeof(cd) * ws_elems));
     CK(cudaMemcpyAsync(d_b, b, sizeof(cd) * m * m, cudaMemcpyHostToDevice, c.st));
-    power_traces_kernel<<<1, 32, 0, c.st>>>(d_b, m, K, backend, cap_mult, d_t, d_ok, d_ws);
+    power_traces_kernel<<<1, 32, 0, c.st>>>(d_b, m, K, backend, cap_mult, d_t, d_ok, d_sw, d_ws);
     ++g_launches;
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(traces, d_t, sizeof(cd) * K, cudaMemcpyDeviceToHost, c.st));
     CK(cudaMemcpyAsync(&h_ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, c.st));
+    CK(cudaMemcpyAsync(&h_sw, d_sw, sizeof(long long), cudaMemcpyDeviceToHost, c.st));
     CK(cudaStreamSynchronize(c.st));
-    *sweeps = -1;  // the QR sweep count is not tracked on the device
+    *sweeps = backend == 0 ? h_sw : 0;  // charpoly: no QR sweeps
     *ok = h_ok;
     return HAFB_OK;
 }

@@ -18,10 +18,8 @@ static cudaError_t launch_one(const cd* at, const cd* dg, int n_half, const Clas
     constexpr int THREADS = TPB * W;
     const size_t smem = (size_t)TPB * MirrorLayout<S>::TOTAL * sizeof(cd);
     auto kern = mirror_term_kernel<S, L>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
     int occ = 1;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, THREADS, smem);
+    cudaError_t e = launch_config((const void*)kern, THREADS, smem, (int)smem, &occ);
     if (e != cudaSuccess) return e;
     const long long want = (ci.n_items + TPB - 1) / TPB;
     const long long cap_blocks = (long long)sms * std::max(occ, 1);

@@ -18,10 +18,8 @@ static cudaError_t launch_one(const uint32_t* at, const uint32_t* dg, int n_half
     constexpr int TPB = kModpThreads / W;
     const size_t smem = (size_t)TPB * ModpLayout<S>::TOTAL * sizeof(uint32_t);
     auto kern = modp_term_kernel<S, L>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
     int occ = 1;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kModpThreads, smem);
+    cudaError_t e = launch_config((const void*)kern, kModpThreads, smem, (int)smem, &occ);
     if (e != cudaSuccess) return e;
     ModP M = make_modp(p);
     const long long want = (ci.n_items + TPB - 1) / TPB;

@@ -2,7 +2,8 @@
 // matrix staged in shared memory.  Handles every size s = 2|Z| <= 62, both
 // backends (charpoly / spectral), with and without loop terms, in MIRROR
 // arithmetic (bit-identical to the reference).  The register-resident kernels
-// in term_reg.cuh take over the FLOP-heavy sizes; this kernel covers the rest
+// (term_fast.cuh for FAST, term_mirror.cuh for the bit-exact charpoly backend)
+// take over the FLOP-heavy sizes; this kernel covers the rest
 // and is the parity baseline for them.
 //
 // Reference: pkg/src/hafnium/kernels/_numba.py
@@ -224,7 +225,8 @@ __device__ inline void qr_sweep_smem(cd* H, int m, int lo, int hi, cd shift, int
 }
 
 // _numba.py:115-188 after the Hessenberg reduction. returns converged; eig[] filled
-__device__ inline bool hess_eigvals_smem(cd* H, int m, int cap_mult, cd* eig, int lane) {
+__device__ inline bool hess_eigvals_smem(cd* H, int m, int cap_mult, cd* eig, int lane,
+                                         long long* sweeps_out = nullptr) {
 #define HH(r, c) H[(r) * m + (c)]
     for (int i = lane; i < m; i += 32) eig[i] = mk(0.0, 0.0);
     __syncwarp();
@@ -275,7 +277,10 @@ __device__ inline bool hess_eigvals_smem(cd* H, int m, int cap_mult, cd* eig, in
             stagnation = 0;
             continue;
         }
-        if (total >= cap) return false;
+        if (total >= cap) {
+            if (sweeps_out) *sweeps_out = total;
+            return false;
+        }
         stagnation += 1;
         cd shift;
         if (stagnation % 10 == 0) {
@@ -294,6 +299,7 @@ __device__ inline bool hess_eigvals_smem(cd* H, int m, int cap_mult, cd* eig, in
         total += 1;
     }
     __syncwarp();
+    if (sweeps_out) *sweeps_out = total;
     return true;
 #undef HH
 }

@@ -172,7 +172,8 @@ def batch_raw(a, n_half, backend, include_loops, n_ranges, symmetry_rtol,
 
 def power_traces_spectral(b, K, cap_mult=SWEEP_CAP_MULT, *, device=None):
     """(traces, sweeps, converged); destroys nothing (the device works on a copy).
-    Replaces _numba.py:415-422.  Sweeps are reported as -1 (not tracked)."""
+    Replaces _numba.py:415-422: sweeps is the QR sweep count of the device iteration
+    (identical to the reference's, which it replays operation for operation)."""
     lib = _lib.load(require_device=True)
     h = _lib.c128(b)
     out = np.zeros(K, np.complex128)

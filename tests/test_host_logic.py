@@ -160,3 +160,10 @@ def test_more_devices_than_visible_is_a_clear_error(monkeypatch):
     monkeypatch.setattr(kernels, "device_count", lambda: 2)
     with pytest.raises(DeviceError, match="devices=4"):
         engine.hafnian(workloads.cfg0(), backend="charpoly", devices=4)
+
+
+def test_fast_arith_requires_charpoly_backend():
+    with pytest.raises(ValueError, match="charpoly"):
+        engine.EngineOptions(backend="spectral", arith="fast").validate()
+    engine.EngineOptions(backend="charpoly", arith="fast").validate()
+    engine.EngineOptions(backend="spectral", arith="mirror").validate()

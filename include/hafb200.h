@@ -23,7 +23,7 @@
  *   - arith: 0 = MIRROR (the reference's exact IEEE operation sequence, results
  *     bit-identical to the reference), 1 = FAST (FMA-contracted kernels).
  *
- * Sizes: n_half = n/2 in [1, 31] (masks are 32-bit on the device).
+ * Sizes: n_half = n/2 in [1, 32] (masks are 32-bit on the device; n <= 64).
  */
 #ifndef HAFB200_H
 #define HAFB200_H
@@ -90,7 +90,7 @@ int hafb_batch(const double* atilde, const double* diag, int batch, int n_half, 
                double* results, int64_t* fails);
 
 /* Replaces power_traces_charpoly / power_traces_spectral (kernels/_numba.py:415-433):
- * traces tr(b^k), k = 1..K of one general m x m complex matrix (m <= 62).
+ * traces tr(b^k), k = 1..K of one general m x m complex matrix (m <= 64).
  * ok: charpoly -> finite flag; spectral -> converged flag.  sweeps: QR sweeps (spectral). */
 int hafb_power_traces(const double* b, int m, int K, int backend, int cap_mult, int arith,
                       int device, double* traces, int64_t* sweeps, int32_t* ok);

@@ -27,7 +27,7 @@ BUILD_ROOT = os.environ.get("HAFB200_BUILD_DIR", os.path.join(REPO, "build"))
 LIB = os.environ.get("HAFB200_LIB") or os.path.join(PKG, "libhafb200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FAST_SIZES = list(range(2, 49, 2))  # kFastSMax = 48 (csrc/fast_launch.h)
-MIRROR_SIZES = list(range(2, 63, 2))  # n <= 62
+MIRROR_SIZES = list(range(2, 65, 2))  # n <= 64 (D <= 32: 32-bit masks)
 
 
 def nvcc() -> str:

@@ -45,7 +45,7 @@ int cuda_fail(const char* what, cudaError_t e) {
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 int check_common(int n_half, int backend, int arith) {
-    if (n_half < 1 || n_half > kMaxHalf) return fail(HAFB_ERR_ARG, "n_half must be in [1, 31]");
+    if (n_half < 1 || n_half > kMaxHalf) return fail(HAFB_ERR_ARG, "n_half must be in [1, 32]");
     if (backend != 0 && backend != 1) return fail(HAFB_ERR_ARG, "backend must be 0 or 1");
     if (arith != 0 && arith != 1) return fail(HAFB_ERR_ARG, "arith must be 0 or 1");
     return HAFB_OK;
@@ -274,7 +274,7 @@ cudaError_t launch_mirror_class(int S, const cd* at, const cd* dg, int n_half,
     case SS: return launch_mirror_S<SS>(L, at, dg, n_half, ci, terms, status, st, sms);
         MC(2) MC(4) MC(6) MC(8) MC(10) MC(12) MC(14) MC(16) MC(18) MC(20) MC(22) MC(24)
         MC(26) MC(28) MC(30) MC(32) MC(34) MC(36) MC(38) MC(40) MC(42) MC(44) MC(46) MC(48)
-        MC(50) MC(52) MC(54) MC(56) MC(58) MC(60) MC(62)
+        MC(50) MC(52) MC(54) MC(56) MC(58) MC(60) MC(62) MC(64)
 #undef MC
         default:
             return cudaErrorInvalidValue;
@@ -355,6 +355,32 @@ int upload_tables(int D, const std::vector<Seg>& segs, void* table_ws, cudaStrea
     return HAFB_OK;
 }
 
+// Forked streams for concurrent small classes: per host thread and device (calls from
+// one thread are sequential, so its events can be re-recorded; other threads have their
+// own), created on first use and kept for the thread's lifetime.
+struct AuxStreams {
+    static constexpr int kN = 4;
+    cudaStream_t s[kN] = {};
+    cudaEvent_t fork = nullptr, join[kN] = {};
+};
+
+AuxStreams* aux_streams() {
+    thread_local AuxStreams per_dev[64];
+    thread_local bool made[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    AuxStreams& a = per_dev[dev];
+    if (!made[dev]) {
+        for (int i = 0; i < AuxStreams::kN; ++i) {
+            if (cudaStreamCreateWithFlags(&a.s[i], cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+            if (cudaEventCreateWithFlags(&a.join[i], cudaEventDisableTiming) != cudaSuccess) return nullptr;
+        }
+        if (cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+        made[dev] = true;
+    }
+    return &a;
+}
+
 // Upload the tables and launch every nonempty class (largest classes first).
 int enqueue_classes(int backend, int arith, const cd* at, const cd* dg, int n_half, const std::vector<Seg>& segs,
                     int batch, long long term_stride, long long at_stride, long long dg_stride,
@@ -364,13 +390,37 @@ int enqueue_classes(int backend, int arith, const cd* at, const cd* dg, int n_ha
     DevTables dt;
     int rc = upload_tables(D, segs, table_ws, st, dt);
     if (rc) return rc;
+    // Classes too small to fill the GPU (a few items per SM) are latency-bound: one
+    // team's serial chain per subset.  They run concurrently on forked streams, so a
+    // small problem costs about its longest class instead of the sum of all classes;
+    // the GPU-filling classes stay in order on `st` (their one-block-per-SM phases
+    // keep the instruction cache warm) and only overlap the small ones.
+    const long long small_items = 16LL * sm_count();
+    AuxStreams* aux = nullptr;
+    int next_aux = 0;
     for (int m = D; m >= 1; --m) {
         if (dt.t.count(m) == 0) continue;
         const ClassItems ci = dt.items(m, batch, term_stride, at_stride, dg_stride);
+        cudaStream_t ls = st;
+        if (ci.n_items <= small_items) {
+            if (!aux) {
+                aux = aux_streams();
+                if (!aux) return fail(HAFB_ERR_CUDA, "auxiliary stream creation failed");
+                CK(cudaEventRecord(aux->fork, st));
+                for (int i = 0; i < AuxStreams::kN; ++i) CK(cudaStreamWaitEvent(aux->s[i], aux->fork, 0));
+            }
+            ls = aux->s[next_aux++ % AuxStreams::kN];
+        }
         cudaError_t e = launch_class(backend, arith, loops, 2 * m, at, dg, n_half, ci, cap, terms,
-                                     status, st);
+                                     status, ls);
         ++g_launches;
         if (e != cudaSuccess) return cuda_fail("fast class launch", e);
+    }
+    if (aux) {  // join: later work on `st` (the range reduction) sees every class's terms
+        for (int i = 0; i < AuxStreams::kN; ++i) {
+            CK(cudaEventRecord(aux->join[i], aux->s[i]));
+            CK(cudaStreamWaitEvent(st, aux->join[i], 0));
+        }
     }
     return HAFB_OK;
 }
@@ -384,7 +434,7 @@ cudaError_t launch_modp_class(int S, bool loops, const uint32_t* at, const uint3
     case SS: return launch_modp_S<SS>(loops, at, dg, n_half, ci, p, inv, total, st, sms);
         PC(2) PC(4) PC(6) PC(8) PC(10) PC(12) PC(14) PC(16) PC(18) PC(20) PC(22) PC(24)
         PC(26) PC(28) PC(30) PC(32) PC(34) PC(36) PC(38) PC(40) PC(42) PC(44) PC(46) PC(48)
-        PC(50) PC(52) PC(54) PC(56) PC(58) PC(60) PC(62)
+        PC(50) PC(52) PC(54) PC(56) PC(58) PC(60) PC(62) PC(64)
 #undef PC
         default:
             return cudaErrorInvalidValue;
@@ -678,7 +728,7 @@ int hafb_sum_range_list(const double* atilde, const double* diag, int n_half, in
 int hafb_sum_subsets_det(const double* atilde, const double* diag, int n_half, int backend,
                          int include_loops, int n_ranges, int cap_mult, int arith, int device,
                          double* partials, int64_t* fails) {
-    if (n_half < 1 || n_half > kMaxHalf) return fail(HAFB_ERR_ARG, "n_half must be in [1, 31]");
+    if (n_half < 1 || n_half > kMaxHalf) return fail(HAFB_ERR_ARG, "n_half must be in [1, 32]");
     if (n_ranges < 1) return fail(HAFB_ERR_ARG, "n_ranges must be >= 1");
     // the standard ranges are the mask-range chunks of [1, 2^D) (same width, same bounds)
     uint64_t total = 1ull << n_half;
@@ -990,7 +1040,7 @@ int hafb_batch_raw(const double* a, int batch, int n_half, int backend, int incl
 int hafb_power_traces(const double* b, int m, int K, int backend, int cap_mult, int arith,
                       int device, double* traces, int64_t* sweeps, int32_t* ok) {
     g_err.clear();
-    if (m < 1 || m > 2 * kMaxHalf) return fail(HAFB_ERR_ARG, "m must be in [1, 62]");
+    if (m < 1 || m > 2 * kMaxHalf) return fail(HAFB_ERR_ARG, "m must be in [1, 64]");
     if (K < 1) return fail(HAFB_ERR_ARG, "K must be >= 1");
     if (backend != 0 && backend != 1) return fail(HAFB_ERR_ARG, "backend must be 0 or 1");
     (void)arith;
@@ -1024,7 +1074,7 @@ int hafb_power_traces(const double* b, int m, int K, int backend, int cap_mult, 
 
 int hafb_charpoly_coefficients(const double* b, int m, int arith, int device, double* coeffs) {
     g_err.clear();
-    if (m < 1 || m > 2 * kMaxHalf) return fail(HAFB_ERR_ARG, "m must be in [1, 62]");
+    if (m < 1 || m > 2 * kMaxHalf) return fail(HAFB_ERR_ARG, "m must be in [1, 64]");
     (void)arith;
     int mm = m + (m & 1);
     Call c;
@@ -1046,7 +1096,7 @@ int hafb_modp_sums(const uint32_t* atilde_p, const uint32_t* diag_p, const uint3
                    int n_primes, int n_half, uint64_t lo, uint64_t hi, int include_loops,
                    int device, uint64_t* residues, double* device_ms) {
     g_err.clear();
-    if (n_half < 1 || n_half > kMaxHalf) return fail(HAFB_ERR_ARG, "n_half must be in [1, 31]");
+    if (n_half < 1 || n_half > kMaxHalf) return fail(HAFB_ERR_ARG, "n_half must be in [1, 32]");
     if (n_primes < 1 || n_primes > 64) return fail(HAFB_ERR_ARG, "n_primes must be in [1, 64]");
     if (hi < lo || hi > (1ull << n_half)) return fail(HAFB_ERR_ARG, "bad mask range");
     const int n = 2 * n_half;

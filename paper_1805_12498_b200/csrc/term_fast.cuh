@@ -74,7 +74,7 @@ constexpr int kGroup = 2;
 #define HAFB_PIVOT_TAU 1.0f
 #endif
 constexpr float kPivotThreshold = HAFB_PIVOT_TAU;  // columns per uniform branch in the Hessenberg sweep
-constexpr int kDMax = 31;
+constexpr int kDMax = 32;  // D = n/2 <= 32
 #ifndef HAFB_SHFL_PIVOT
 #define HAFB_SHFL_PIVOT 1
 #endif

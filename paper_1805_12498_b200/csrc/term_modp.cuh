@@ -96,8 +96,8 @@ inline ModP make_modp(uint32_t p) {
 }
 
 // per-prime constant table (Montgomery form), uploaded by the host
-constexpr int kModpTab = 96;   // [k] = k^-1 R, [32 + k] = k R (k = 1..31)
-constexpr int kModpTabK = 32;
+constexpr int kModpTab = 96;   // [k] = k^-1 R, [48 + k] = k R (k = 1..47; D <= 32)
+constexpr int kModpTabK = 48;
 
 constexpr int kModpThreads = 128;
 

@@ -1,5 +1,5 @@
 // term_smem.cuh -- general subset-term kernel: one warp per subset, the subset
-// matrix staged in shared memory.  Handles every size s = 2|Z| <= 62, both
+// matrix staged in shared memory.  Handles every size s = 2|Z| <= 64, both
 // backends (charpoly / spectral), with and without loop terms, in MIRROR
 // arithmetic (bit-identical to the reference).  The register-resident kernels
 // (term_fast.cuh for FAST, term_mirror.cuh for the bit-exact charpoly backend)
@@ -24,7 +24,7 @@
 
 namespace hafb {
 
-constexpr int kMaxHalf = 31;  // masks are 32-bit on the device; s <= 62
+constexpr int kMaxHalf = 32;  // masks are 32-bit on the device: n <= 64, s <= 64
 constexpr double kDeflationRtol = 1e-14;  // _numba.py:32
 
 // shared-memory footprint (in cd elements) of one warp's workspace for subset

@@ -23,7 +23,7 @@ from . import _lib
 
 SWEEP_CAP_MULT = 30  # _numba.py:33; read at call time by the engine (monkeypatchable)
 DEFLATION_RTOL = 1e-14  # _numba.py:32 (compiled into the kernels)
-MAX_HALF = 31  # device masks are 32-bit
+MAX_HALF = 32  # device masks are 32-bit: n <= 64
 
 ARITH_MODES = {"mirror": 0, "fast": 1}
 

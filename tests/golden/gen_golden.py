@@ -206,6 +206,33 @@ def gen_batch(count: int = 4096):
     np.savez_compressed(os.path.join(HERE, "batch_cfg1.npz"), **out)
 
 
+def gen_range_n64():
+    """n = 64 (D = 32, the device's 32-bit-mask limit): the identical range [0, 2^20) and
+    per-term values for sampled masks of the large classes (S = 42..64)."""
+    out = {}
+    A = W.cfg4(5, 64)
+    at, dg, nh = _prepare(A, False)
+    out["n64s5/A"] = A
+    t0 = time.time()
+    sums, fails = _range_driver(at, dg, nh, 0, 1 << 20, 512, 1, False, nb.SWEEP_CAP_MULT)
+    out["n64s5/partials_b1"] = sums
+    out["n64s5/fails_b1"] = fails
+    out["n64s5/result_b1"] = np.array(tree_reduce(sums))
+    rng = np.random.default_rng(64)
+    masks = []
+    for m in (21, 24, 27, 30, 31, 32):
+        for _ in range(3 if m < 32 else 1):
+            bits = rng.choice(nh, size=m, replace=False)
+            masks.append(int(np.sum(np.left_shift(np.uint64(1), bits.astype(np.uint64)))))
+    masks = np.array(sorted(set(masks)), dtype=np.uint64)
+    vals, st = ref_terms(at, dg, nh, masks, 1, False)
+    out["n64s5/masks"] = masks
+    out["n64s5/terms_b1"] = vals
+    out["n64s5/status_b1"] = st
+    print(f"range n64s5: {tree_reduce(sums)} {time.time() - t0:.1f}s", flush=True)
+    np.savez_compressed(os.path.join(HERE, "range_n64.npz"), **out)
+
+
 def gen_powertraces():
     out = {}
     rng = np.random.default_rng(2024)
@@ -243,3 +270,5 @@ if __name__ == "__main__":
         gen_range_n52()
     if "batch" in which:
         gen_batch()
+    if "range_n64" in which:
+        gen_range_n64()

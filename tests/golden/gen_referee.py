@@ -12,7 +12,8 @@ against a value ~2000x more precise than any of them.
 
 * referee.npz          cfg0, cfg2 (loops), cfg3, cfg1 seeds 0..3: full results;
                        the n=52 / n=56 identical ranges [0, 2^20) (seeds 3, 4);
-                       per-term referee values for the terms.npz masks
+                       per-term referee values for the terms.npz masks;
+                       n = 64 (range_n64.npz): the range and its large-class terms
 * referee_batch.npz    the 4096-matrix cfg1 batch (per matrix; input digests as
                        in batch_cfg1.npz)
 * referee_full52.npz   the FULL n=52 seed-3 hafnian (2^26-1 terms, ~1 h on 8 cores)
@@ -75,7 +76,14 @@ def gen_small(out):
 
 
 def gen_ranges(out):
-    for name, c in _cases("range_n52.npz").items():
+    cases = dict(_cases("range_n52.npz"))
+    if os.path.exists(os.path.join(HERE, "range_n64.npz")):
+        n64 = _cases("range_n64.npz")
+        cases.update(n64)
+        for name, c in n64.items():  # per-term referee values of the large-class masks
+            at, dg, nh = engine._prepare(c["A"], False)
+            out[f"terms_{name}/values"] = R.terms(at, dg, nh, c["masks"], False)
+    for name, c in cases.items():
         at, dg, nh = engine._prepare(c["A"], False)
         t0 = time.time()
         hi, lo, sa = R.sum_range(at, dg, nh, 0, 1 << 20, False)

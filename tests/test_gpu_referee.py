@@ -47,11 +47,12 @@ def test_whole_problem_vs_referee(name, arith):
         assert abs(got.real - exact) <= abs(complex(c["result_b1"]).real - exact) or arith == "mirror"
 
 
-@pytest.mark.parametrize("name", ["n52s3", "n52s4", "n56s4"])
+@pytest.mark.parametrize("name", ["n52s3", "n52s4", "n56s4", "n64s5"])
 def test_identical_range_vs_referee(name):
-    """North-star parity for n >= 48: masks [0, 2^20) of the n=52 / n=56 inputs (seeds 3, 4)."""
+    """North-star parity for n >= 48: masks [0, 2^20) of the n=52 / n=56 inputs (seeds 3, 4)
+    and of an n=64 input (seed 5; D = 32, the 32-bit-mask limit)."""
     ref = load_golden("referee.npz")
-    case = load_golden("range_n52.npz")[name]
+    case = load_golden("range_n64.npz" if name == "n64s5" else "range_n52.npz")[name]
     hi, lo, sa = _truth(ref, f"range_{name}")
     at, dg, nh = engine._prepare(case["A"], False)
     for arith in ("fast", "mirror"):
@@ -132,3 +133,22 @@ def test_full_n52_vs_referee():
     for arith in ("fast", "mirror"):
         got = engine.hafnian(A, backend="charpoly", arith=arith)
         assert accuracy.within(got, hi, lo, sa), (arith, accuracy.error(got, hi, lo) / abs(hi))
+
+
+def test_n64_large_class_terms():
+    """n = 64: sampled subsets of the large classes (S = 42..64, incl. the full mask),
+    MIRROR bit-identical to the reference's terms, FAST within the reference's per-term
+    error against the referee."""
+    c = load_golden("range_n64.npz")["n64s5"]
+    truth = load_golden("referee.npz")["terms_n64s5"]["values"]
+    at, dg, nh = engine._prepare(c["A"], False)
+    assert nh == 32
+    mir, st = kernels.terms(at, dg, nh, c["masks"], 1, False, arith="mirror")
+    assert not st.any()
+    assert (mir.view(np.uint64) == c["terms_b1"].view(np.uint64)).all()
+    fast, st = kernels.terms(at, dg, nh, c["masks"], 1, False, arith="fast")
+    assert not st.any()
+    sc = np.abs(truth)
+    ef = np.max(np.abs(fast - truth) / sc)
+    er = np.max(np.abs(c["terms_b1"] - truth) / sc)
+    assert ef <= 4 * er + 1e-15, (ef, er)

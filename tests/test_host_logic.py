@@ -77,7 +77,8 @@ def test_input_semantics():
     with pytest.raises(OddDimension):
         engine._prepare(np.zeros((3, 3)), False)
     with pytest.raises(TooLarge):
-        engine._prepare(np.zeros((64, 64)), False)
+        engine._prepare(np.zeros((66, 66)), False)
+    assert engine._prepare(np.zeros((64, 64)), False)[2] == 32  # n = 64: D = 32 (32-bit masks)
     x = np.arange(16).reshape(4, 4).astype(complex)
     assert np.array_equal(pair_swap(x), x[[1, 0, 3, 2]])
     assert PairSubset(0b101, 3).vertex_indices().tolist() == [0, 1, 4, 5]

@@ -20,7 +20,7 @@ struct Seg {
 
 // Items of one popcount class over a segment list (and over `batch` problems).
 struct ClassItems {
-    const unsigned long long* binom;    // [33][33] table of C(b, p)
+    unsigned long long c_top;           // C(D-1, m): the unranking's first binomial
     const Seg* segs;
     const long long* prefix;            // nseg+1: # class-m masks before segment s
     const unsigned long long* base;     // nseg: # class-m integers below segs[s].lo
@@ -33,18 +33,28 @@ struct ClassItems {
     long long at_stride, dg_stride;     // input offsets between problems (in cd)
     const uint32_t* mlist;              // explicit-mask mode: the class's masks ...
     const long long* mout;              // ... and their buffer indices (else null)
+    Seg seg0;                           // nseg == 1: the segment and its base by value
+    unsigned long long base0;           // (no dependent loads for the first item)
 };
 
-// the r-th (0-based) integer with popcount m, bits below D
-__device__ __forceinline__ uint32_t unrank_mask(const unsigned long long* __restrict__ binom,
-                                                unsigned long long r, int m, int D) {
+// the r-th (0-based) integer with popcount m, bits below D (combinatorial number
+// system).  The binomials are stepped arithmetically from c_top = C(D-1, m):
+//   C(b-1, m) = C(b, m) (b - m) / b,   C(b-1, m-1) = C(b, m) m / b,
+// exact in double (every value is an integer < 2^36 and the quotient is exact), so
+// unranking issues no memory loads: a table lookup per bit is a chain of ~D dependent
+// global-memory round trips, which made the first item of every launch cost ~15 us.
+__device__ __forceinline__ uint32_t unrank_mask(unsigned long long r, int m, int D,
+                                                unsigned long long c_top) {
     uint32_t mask = 0;
+    double c = (double)c_top;  // C(b, m) for the current b
     for (int b = D - 1; b >= 0 && m > 0; --b) {
-        unsigned long long c = __ldg(binom + b * 33 + m);
-        if (r >= c) {
+        if ((double)r >= c) {
             mask |= 1u << b;
-            r -= c;
+            r -= (unsigned long long)c;
+            c = b > 0 ? (c * (double)m) / (double)b : 0.0;
             --m;
+        } else {
+            c = b > 0 ? (c * (double)(b - m)) / (double)b : 0.0;
         }
     }
     return mask;
@@ -65,6 +75,11 @@ __device__ __forceinline__ ItemRef resolve_item(const ClassItems& ci, long long 
         r.out = r.problem * ci.term_stride + ci.mout[rho];
         return r;
     }
+    if (ci.nseg == 1) {
+        r.mask = unrank_mask(ci.base0 + (unsigned long long)rho, ci.m, ci.D, ci.c_top);
+        r.out = r.problem * ci.term_stride + ci.seg0.out_off + (long long)(r.mask - ci.seg0.lo);
+        return r;
+    }
     int lo = 0, hi = ci.nseg - 1;
     while (lo < hi) {  // last s with prefix[s] <= rho
         int mid = (lo + hi + 1) >> 1;
@@ -72,15 +87,15 @@ __device__ __forceinline__ ItemRef resolve_item(const ClassItems& ci, long long 
         else hi = mid - 1;
     }
     const Seg sg = ci.segs[lo];
-    r.mask = unrank_mask(ci.binom, ci.base[lo] + (unsigned long long)(rho - ci.prefix[lo]), ci.m, ci.D);
+    r.mask = unrank_mask(ci.base[lo] + (unsigned long long)(rho - ci.prefix[lo]), ci.m, ci.D, ci.c_top);
     r.out = r.problem * ci.term_stride + sg.out_off + (long long)(r.mask - sg.lo);
     return r;
 }
 
 // Sequential walk over consecutive items of a class.  Inside one segment of one
 // problem, class rank rho+1 is the next larger integer of popcount m (colex order),
-// obtained from the current mask by Gosper's step; the full unranking (a chain of
-// ~D dependent table loads) runs only at the first item and at segment/problem edges.
+// obtained from the current mask by Gosper's step; the full unranking (~D dependent
+// double divisions) runs only at the first item and at segment/problem edges.
 struct ItemCursor {
     long long next = -1;      // the item that continues the walk
     long long item_end = -1;  // first item outside the current segment (or problem)
@@ -105,6 +120,11 @@ __device__ __forceinline__ ItemRef cursor_item(const ClassItems& ci, long long i
     cur.ref = resolve_item(ci, item);
     if (!ci.mlist) {
         const long long p0 = cur.ref.problem * ci.per_problem;
+        if (ci.nseg == 1) {
+            cur.item_end = p0 + ci.per_problem;
+            cur.delta = cur.ref.out - (long long)cur.ref.mask;
+            return cur.ref;
+        }
         const long long rho = item - p0;
         int lo = 0, hi = ci.nseg - 1;
         while (lo < hi) {

@@ -81,8 +81,9 @@ cudaError_t library_pool(int device, cudaMemPool_t* out) {
     return cudaSuccess;
 }
 
-// One host call: its own non-blocking stream and stream-ordered allocations,
-// released (after a stream sync) when the call returns on any path.
+// One host call: the calling thread's non-blocking stream for the device and
+// stream-ordered allocations, released (after a stream sync) when the call returns
+// on any path.
 struct Call {
     cudaStream_t st = nullptr;
     std::vector<void*> bufs;
@@ -91,7 +92,16 @@ struct Call {
         if (e != cudaSuccess) return e;
         e = library_pool(device, &pool);
         if (e != cudaSuccess) return e;
-        return cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+        // one non-blocking stream per (host thread, device), reused across calls
+        // (creating and destroying a stream per call cost ~20 us of a small problem)
+        thread_local cudaStream_t streams[64] = {};
+        if (device < 0 || device >= 64) return cudaErrorInvalidDevice;
+        if (!streams[device]) {
+            e = cudaStreamCreateWithFlags(&streams[device], cudaStreamNonBlocking);
+            if (e != cudaSuccess) return e;
+        }
+        st = streams[device];
+        return cudaSuccess;
     }
     cudaMemPool_t pool = nullptr;
     template <class T>
@@ -106,7 +116,6 @@ struct Call {
         if (!st) return;
         for (void* p : bufs) cudaFreeAsync(p, st);
         cudaStreamSynchronize(st);
-        cudaStreamDestroy(st);
     }
 };
 
@@ -301,7 +310,7 @@ bool use_class_path(int backend) { return backend == 0 || backend == 1; }
 // Device copies of the class-enumeration tables (carved from `table_ws`).
 struct DevTables {
     ClassTables t;
-    unsigned long long* binom = nullptr;
+    Seg seg0 = {0, 0, 0};  // host copy of the first segment
     Seg* segs = nullptr;
     long long* prefix = nullptr;
     unsigned long long* base = nullptr;
@@ -312,7 +321,9 @@ struct DevTables {
         ClassItems ci;
         ci.mlist = nullptr;
         ci.mout = nullptr;
-        ci.binom = binom;
+        ci.c_top = g_binom_host[t.D - 1][m];
+        ci.seg0 = t.nseg == 1 ? seg0 : Seg{0, 0, 0};
+        ci.base0 = t.nseg == 1 ? t.base[(size_t)m] : 0;
         ci.segs = segs;
         ci.prefix = prefix + (size_t)m * (nseg + 1);
         ci.base = base + (size_t)m * nseg;
@@ -330,10 +341,9 @@ struct DevTables {
 
 int upload_tables(int D, const std::vector<Seg>& segs, void* table_ws, cudaStream_t st, DevTables& dt) {
     dt.t = build_tables(D, segs);
+    if (!segs.empty()) dt.seg0 = segs[0];
     const size_t nseg = segs.size();
     char* p = static_cast<char*>(table_ws);
-    dt.binom = reinterpret_cast<unsigned long long*>(p);
-    p += align256(sizeof(g_binom_host));
     dt.segs = reinterpret_cast<Seg*>(p);
     p += align256(sizeof(Seg) * nseg);
     dt.prefix = reinterpret_cast<long long*>(p);
@@ -346,7 +356,6 @@ int upload_tables(int D, const std::vector<Seg>& segs, void* table_ws, cudaStrea
     std::vector<char> img(total);
     char* h = img.data();
     auto at_ = [&](const void* dptr) { return h + (static_cast<const char*>(dptr) - static_cast<char*>(table_ws)); };
-    std::memcpy(at_(dt.binom), g_binom_host, sizeof(g_binom_host));
     std::memcpy(at_(dt.segs), segs.data(), sizeof(Seg) * nseg);
     std::memcpy(at_(dt.prefix), dt.t.prefix.data(), sizeof(long long) * dt.t.prefix.size());
     std::memcpy(at_(dt.base), dt.t.base.data(), sizeof(unsigned long long) * dt.t.base.size());
@@ -442,7 +451,7 @@ cudaError_t launch_modp_class(int S, bool loops, const uint32_t* at, const uint3
 }
 
 size_t table_ws_bytes(int n_half, size_t nseg) {
-    return align256(sizeof(g_binom_host)) + align256(sizeof(Seg) * nseg) + align256(sizeof(long long) * (n_half + 1) * (nseg + 1)) +
+    return align256(sizeof(Seg) * nseg) + align256(sizeof(long long) * (n_half + 1) * (nseg + 1)) +
            align256(sizeof(unsigned long long) * (n_half + 1) * nseg);
 }
 

@@ -61,7 +61,7 @@ static cudaError_t launch_one(const cd* at, const cd* dg, int n_half, const Clas
     constexpr int W = FastTeam<S, L, SH>::W;
     constexpr int NT = NSX ? HAFB_NSX_THREADS : threads_for(S);
     constexpr int TPB = NT / W;
-    const size_t base_smem = (size_t)TPB * FastLayout<S, SH, L>::TOTAL * sizeof(cd) + (kDMax + 1) * sizeof(double);
+    const size_t base_smem = (size_t)TPB * FastLayout<S, SH, L>::TOTAL * sizeof(cd) + kInvSlots * sizeof(double);
     // the one-block-per-SM register classes stage Atilde in shared memory when it fits
     const int n = 2 * n_half;
     const size_t a_bytes = (size_t)n * (n + 1) * sizeof(cd);

@@ -75,6 +75,10 @@ constexpr int kGroup = 2;
 #endif
 constexpr float kPivotThreshold = HAFB_PIVOT_TAU;  // columns per uniform branch in the Hessenberg sweep
 constexpr int kDMax = 32;  // D = n/2 <= 32
+// doubles reserved for the 1/k table in front of the staged Atilde: an even count keeps
+// Atilde 16-byte aligned (an 8-byte-aligned complex array loses LDS.128 and, at S = 28,
+// cost 300 B of register spills and 13 % of the step)
+constexpr int kInvSlots = (kDMax + 2) & ~1;
 #ifndef HAFB_SHFL_PIVOT
 #define HAFB_SHFL_PIVOT 1
 #endif
@@ -99,6 +103,9 @@ constexpr int kDMax = 32;  // D = n/2 <= 32
 #endif
 #ifndef HAFB_QSERIES
 #define HAFB_QSERIES 1
+#endif
+#ifndef HAFB_QS_FOLD
+#define HAFB_QS_FOLD 0
 #endif
 #ifndef HAFB_NS_HI
 #define HAFB_NS_HI 32
@@ -1082,7 +1089,7 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
     // Atilde staged in shared memory (row stride n+1: the lanes' rows fall in distinct
     // banks) for the block's first problem; the subset gathers then read shared memory
     // instead of issuing S scattered global loads per lane
-    cd* As = reinterpret_cast<cd*>(INV + kDMax + 1);
+    cd* As = reinterpret_cast<cd*>(INV + kInvSlots);
     const int ldA = n + 1;
     long long staged_problem = -1;
     const long long block_first = (long long)blockIdx.x * TPB * chunk;
@@ -1357,6 +1364,35 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
 #pragma unroll
             for (int r = 0; r < R; ++r) acc[r] = mk(0.0, 0.0);
             const int src0 = ((int)(threadIdx.x & 31) & ~(W - 1));
+#if HAFB_QS_FOLD
+            // the recurrence's serial chain is broadcast -> multiply-add per step: the scale
+            // -1/m of g_m and the weight (k+m)/2 are folded into the coefficient a_j off
+            // the chain (acc_k += [a_j (k+m)/2 (-1/m)] P_m, with P_m = -m g_m the pushed sum)
+            for (int m = 0; m < D; ++m) {
+                cd pm;
+                if (m == 0) {
+                    pm = mk(1.0, 0.0);
+                } else {
+                    const int chunk = (m - 1) / W;
+                    cd v = acc[0];
+#pragma unroll
+                    for (int r = 1; r < R; ++r)
+                        if (r == chunk) v = acc[r];
+                    pm.re = __shfl_sync(tc.wmask, v.re, src0 + (m - 1) % W);
+                    pm.im = __shfl_sync(tc.wmask, v.im, src0 + (m - 1) % W);
+                }
+                const double sc = m == 0 ? 1.0 : -INV[m];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int k = lane + 1 + W * r;
+                    const int j = k - m;
+                    const bool on = k <= D && j >= 1 && j <= S;
+                    const double wgt = on ? 0.5 * (double)(k + m) * sc : 0.0;
+                    const cd aj = A[S - (on ? j : 1)];
+                    acc[r] = f_cma(acc[r], mk(wgt * aj.re, wgt * aj.im), pm);
+                }
+            }
+#else
             for (int m = 0; m < D; ++m) {
                 cd gm;
                 if (m == 0) {
@@ -1381,6 +1417,7 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
                     acc[r] = f_cma(acc[r], A[S - (on ? j : 1)], mk(wgt * gm.re, wgt * gm.im));
                 }
             }
+#endif
             for (int i = lane; i <= S; i += W) {
                 const cd a = A[i];
                 if (!isfinite(a.re) || !isfinite(a.im)) bad = 1;

@@ -407,21 +407,26 @@ __device__ inline void subset_term_smem(const cd* __restrict__ atilde, const cd*
             __syncwarp();
         }
     }
-    // _exp_top (_numba.py:276-294): lane d owns E[d]; each F[d] is a sequential sum
+    // _exp_top (_numba.py:276-294): lane d owns E[d] (and E[d + 32]: D = 32 needs 33
+    // coefficients); each F[d] is a sequential sum
     const int D = K;
-    if (lane <= D) w.E[lane] = (lane == 0) ? mk(1.0, 0.0) : mk(0.0, 0.0);
+    for (int d = lane; d <= D; d += 32) w.E[d] = (d == 0) ? mk(1.0, 0.0) : mk(0.0, 0.0);
     __syncwarp();
     for (int j = D; j > 0; --j) {
         double inv = r_div(1.0, (double)j);
-        cd f = mk(0.0, 0.0);
-        if (lane <= D) {
-            cd acc = mk(0.0, 0.0);
-            for (int tt = 1; tt <= lane; ++tt) acc = m_add(acc, m_mul(w.E[lane - tt], w.s[tt]));
-            f = m_rmul(inv, acc);
-            if (lane == 0) f = m_add(f, mk(1.0, 0.0));
+        cd f[2] = {mk(0.0, 0.0), mk(0.0, 0.0)};
+        for (int q = 0; q < 2; ++q) {
+            const int d = lane + 32 * q;
+            if (d <= D) {
+                cd acc = mk(0.0, 0.0);
+                for (int tt = 1; tt <= d; ++tt) acc = m_add(acc, m_mul(w.E[d - tt], w.s[tt]));
+                f[q] = m_rmul(inv, acc);
+                if (d == 0) f[q] = m_add(f[q], mk(1.0, 0.0));
+            }
         }
         __syncwarp();
-        if (lane <= D) w.E[lane] = f;
+        for (int q = 0; q < 2; ++q)
+            if (lane + 32 * q <= D) w.E[lane + 32 * q] = f[q];
         __syncwarp();
     }
     cd coeff = w.E[D];

@@ -1039,6 +1039,10 @@ __device__ __forceinline__ void nsx_hessenberg(cd (&w)[S], cd (&ex)[S - 32], int
 }
 
 // team width of the FAST kernel: NSX sizes (no loops) run one-warp teams
+}  // namespace hafb
+#include "charpoly_mma.cuh"
+namespace hafb {
+
 template <int S, bool LOOPS, bool SH>
 struct FastTeam {
     static constexpr bool NSX = nsx_variant(S) && !LOOPS && !SH;
@@ -1235,7 +1239,12 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
         if constexpr (PSYNC) __syncthreads();
         tc.sync();
         // ---------------------------------------------- charpoly (_numba.py:203-225)
-        {
+        // one-warp register classes: blocked, the old-polynomial part on the FP64 tensor
+        // cores (charpoly_mma.cuh); otherwise lane d owns coefficient d of every P_k
+        constexpr bool CPMMA = HAFB_CP_MMA && W == 32 && !NSX && !SH && S >= 18;
+        if constexpr (CPMMA) {
+            charpoly_mma<S, L>(ws, lane);
+        } else {
             const cd* Hs = ws + L::HS;
             // h(i, c) of the Hessenberg form: packed store, or (SH) the matrix in smem
             // with logical row i in lane lm[i]

@@ -32,7 +32,7 @@ int main(int argc, char** argv) {
     cudaMemcpy(d_pre, prefix, 16, cudaMemcpyHostToDevice);
     cudaMemcpy(d_base, base, 8, cudaMemcpyHostToDevice);
     cudaMemcpy(d_binom, B, sizeof(B), cudaMemcpyHostToDevice);
-    ClassItems ci{d_binom, d_seg, d_pre, d_base, 1, m, D, prefix[1], prefix[1], 0, 0, 0, nullptr, nullptr};
+    ClassItems ci{B[D - 1][m], d_seg, d_pre, d_base, 1, m, D, prefix[1], prefix[1], 0, 0, 0, nullptr, nullptr, sg, base[0]};
     #ifndef NTV
 #define NTV kFastThreads
 #endif
@@ -41,7 +41,7 @@ int main(int argc, char** argv) {
 #define SHV true
 #endif
     const int stage = (NTV > kFastThreads && !SHV) ? 1 : 0;
-    size_t smem = (size_t)TPB * FastLayout<HAFB_S, SHV, false>::TOTAL * sizeof(cd) + (kDMax + 1) * 8 + (stage ? (size_t)n * (n + 1) * sizeof(cd) : 0);
+    size_t smem = (size_t)TPB * FastLayout<HAFB_S, SHV, false>::TOTAL * sizeof(cd) + kInvSlots * 8 + (stage ? (size_t)n * (n + 1) * sizeof(cd) : 0);
     auto k = fast_term_kernel<HAFB_S, false, SHV, NTV>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int occ; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NTV, smem);

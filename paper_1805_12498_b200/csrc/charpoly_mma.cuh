@@ -84,7 +84,10 @@ __device__ __forceinline__ cd cp_pval(const cd* ws, int m, int d) {
 // Coefficients of P_S into ws[L::A + 0..S] (A[S] = 1).  One full warp (W = 32, S <= 32).
 template <int S, class L>
 __device__ __forceinline__ void charpoly_mma(cd* ws, const int lane) {
-    static_assert(S <= 32, "one coefficient per lane");
+    // lane d owns coefficient d; for S > 32 (the NSX classes) lanes < E = S - 32 also own
+    // coefficient 32 + lane (non-zero only in P_k, k >= 32: the last block's rows)
+    static_assert(S <= 40, "at most two coefficients per lane");
+    constexpr int E = S > 32 ? S - 32 : 0;
     using PL = CpPlan<S>;
     static_assert(PL::tb_max() <= L::RED - L::PR, "T staging exceeds the dead scratch");
     cd* Hs = ws + L::HS;
@@ -113,6 +116,20 @@ __device__ __forceinline__ void charpoly_mma(cd* ws, const int lane) {
             if (on) *p = c;
             return true;
         });
+        if constexpr (E > 0) {  // rows m = 32 + lane
+            cd prodx = mk(1.0, 0.0);
+            static_for<34, S + 1>([&](auto kk) {
+                constexpr int k = decltype(kk)::value;
+                const bool on = lane < E && 32 + lane <= k - 2;
+                const cd np = f_mul(32 + lane == k - 2 ? mk(1.0, 0.0) : prodx, bt[k - 1]);
+                prodx = mk(on ? np.re : prodx.re, on ? np.im : prodx.im);
+                cd* p = Hs + pk_at(k - 1, on ? 32 + lane : 0);
+                const cd h = *p;
+                const cd c = f_mul(h, prodx);
+                if (on) *p = c;
+                return true;
+            });
+        }
     }
     __syncwarp();
     HT_MARK(5);
@@ -162,6 +179,7 @@ __device__ __forceinline__ void charpoly_mma(cd* ws, const int lane) {
         HT_MARK(6);
         // ---- the block's rows, lane d = coefficient d
         cd Pb[R];
+        cd Pb2[E > 0 ? R : 1];  // coefficient 32 + lane (lanes < E)
         static_for<0, R>([&](auto jj) {
             constexpr int j = decltype(jj)::value;
             constexpr int k = K + j;
@@ -202,6 +220,30 @@ __device__ __forceinline__ void charpoly_mma(cd* ws, const int lane) {
                 Pb[j] = acc;
                 if constexpr (k == S) {
                     if (lane < S) A[lane] = acc;
+                }
+                if constexpr (E > 0) {
+                    // P_k[32 + lane]: zero below k = 32; no old part (P_m[d] = 0 for m < K <= 32 <= d)
+                    if constexpr (k < 32) {
+                        Pb2[j] = mk(0.0, 0.0);
+                    } else {
+                        const cd pk2 = j == 0 ? mk(0.0, 0.0) : Pb2[j == 0 ? 0 : j - 1];
+                        cd q, w31;
+                        q.re = __shfl_up_sync(0xffffffffu, pk2.re, 1);
+                        q.im = __shfl_up_sync(0xffffffffu, pk2.im, 1);
+                        w31.re = __shfl_sync(0xffffffffu, pk1.re, 31);
+                        w31.im = __shfl_sync(0xffffffffu, pk1.im, 31);
+                        if (lane == 0) q = w31;  // P_{k-1}[31]
+                        constexpr int M2 = K > 32 ? K : 32;
+                        static_for<M2, k>([&](auto mm) {
+                            constexpr int m = decltype(mm)::value;
+                            q = f_cms(q, Hs[pk_at(k - 1, m)], Pb2[m - K]);
+                            return true;
+                        });
+                        Pb2[j] = q;
+                        if constexpr (k == S) {
+                            if (lane < E) A[32 + lane] = q;
+                        }
+                    }
                 }
             }
             return true;

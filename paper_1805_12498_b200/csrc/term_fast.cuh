@@ -1241,7 +1241,7 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
         // ---------------------------------------------- charpoly (_numba.py:203-225)
         // one-warp register classes: blocked, the old-polynomial part on the FP64 tensor
         // cores (charpoly_mma.cuh); otherwise lane d owns coefficient d of every P_k
-        constexpr bool CPMMA = HAFB_CP_MMA && W == 32 && !NSX && !SH && S >= 18;
+        constexpr bool CPMMA = HAFB_CP_MMA && W == 32 && !SH && S >= 18 && S <= 40;
         if constexpr (CPMMA) {
             charpoly_mma<S, L>(ws, lane);
         } else {

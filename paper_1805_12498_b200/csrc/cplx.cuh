@@ -85,6 +85,11 @@ HD cd m_rdiv(cd a, double r) { return m_div(a, mk(r, 0.0)); }
 // glibc >= 2.35 __hypot (sysdeps/ieee754/dbl-64/e_hypot.c, non-FMA kernel), which is
 // what numba's abs(complex) calls on this image.  Verified bit-exact against the
 // host libm in tests/test_cplx_host.py.
+// Attribution: the algorithm (scaling ranges and the correction terms below) is the
+// one published in GNU C Library's e_hypot.c (LGPL-2.1-or-later, by Adhemerval
+// Zanella / the glibc authors, after Borges' "An Improved Algorithm for hypot(a,b)");
+// it is restated here operation by operation because bit-identity with the reference
+// requires the same rounding sequence.
 HD double hypot_kernel(double ax, double ay) {
     double h = r_sqrt(r_add(r_mul(ax, ax), r_mul(ay, ay)));
     double t1, t2;
@@ -124,7 +129,8 @@ HD double m_hypot(double x, double y) {
 }
 HD double m_abs(cd a) { return m_hypot(a.re, a.im); }
 
-// numba cmathimpl.sqrt_impl (NumPy npy_csqrt, CACM algorithm 312)
+// numba cmathimpl.sqrt_impl (NumPy npy_csqrt, CACM algorithm 312; BSD-licensed NumPy
+// algorithm restated for bit-identity)
 HD cd m_sqrt(cd z) {
     const double THRES = 1.7976931348623157e308 / (1. + 1.414213562373095048801688724209698079E0);
     double a = z.re, b = z.im;

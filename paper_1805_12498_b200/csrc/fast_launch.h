@@ -19,8 +19,11 @@ namespace hafb {
 // concurrent host threads never race on it) and the occupancy.  The two runtime
 // queries cost tens of microseconds per launch, which dominated small problems (a
 // hafnian of n = 20 is ~12 launches of a few microseconds each).
+// carveout >= 0: the kernel's preferred shared-memory carveout (percent of the unified
+// L1/shared array); the small-block shared-memory kernels ask for the maximum, else the
+// driver may pick a smaller shared-memory configuration and cap their teams per SM
 inline cudaError_t launch_config(const void* kern, int threads, size_t smem, int smem_attr,
-                                 int* occ) {
+                                 int* occ, int carveout = -1) {
     struct Entry {
         const void* k;
         int dev, threads;
@@ -42,6 +45,10 @@ inline cudaError_t launch_config(const void* kern, int threads, size_t smem, int
     }
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_attr);
     if (e != cudaSuccess) return e;
+    if (carveout >= 0) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+        if (e != cudaSuccess) return e;
+    }
     int o = 1;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, smem);
     if (e != cudaSuccess) return e;

@@ -19,7 +19,10 @@ static cudaError_t launch_one(const cd* at, const cd* dg, int n_half, const Clas
     const size_t smem = (size_t)TPB * MirrorLayout<S>::TOTAL * sizeof(cd);
     auto kern = mirror_term_kernel<S, L>;
     int occ = 1;
-    cudaError_t e = launch_config((const void*)kern, THREADS, smem, (int)smem, &occ);
+    #ifndef HAFB_MIRROR_CARVEOUT
+#define HAFB_MIRROR_CARVEOUT 100
+#endif
+    cudaError_t e = launch_config((const void*)kern, THREADS, smem, (int)smem, &occ, HAFB_MIRROR_CARVEOUT);
     if (e != cudaSuccess) return e;
     const long long want = (ci.n_items + TPB - 1) / TPB;
     const long long cap_blocks = (long long)sms * std::max(occ, 1);

@@ -36,6 +36,16 @@ constexpr int kMirrorThreads = 64;
 #ifndef MIRROR_HS_UNROLL
 #define MIRROR_HS_UNROLL 1
 #endif
+// minimum resident 64-thread blocks per SM the register allocation must allow: 8 caps
+// the kernel at 128 registers (16 warps/SM); left free, ptxas spent 255 at S = 28..32
+// and registers, not shared memory, capped the teams per SM
+#ifndef HAFB_MIRROR_MINB
+#define HAFB_MIRROR_MINB 8
+#endif
+template <int S>
+constexpr int mirror_minb() {
+    return TeamWidth<S>::W >= 32 ? HAFB_MIRROR_MINB : 1;  // 16-lane teams spill at 128
+}
 constexpr int kMirrorCpUnroll = MIRROR_CP_UNROLL;  // charpoly i-loop unroll
 constexpr int kMirrorHsUnroll = MIRROR_HS_UNROLL;  // Hessenberg column-loop unroll
 
@@ -50,27 +60,32 @@ constexpr int mirror_tpb() {
 template <int S>
 struct MirrorLayout {
     static constexpr int LD = S + 1;                     // odd column stride: conflict-free
-    static constexpr int TRI = (S + 1) * (S + 2) / 2;    // triangular tables
-    // region A: the S x S subset matrix during the Hessenberg reduction, then (after
-    // the reduced form is packed into HS) the charpoly tables CF and P
-    static constexpr int AREA = S * LD > (S + 1) * (S + 1) ? S * LD : (S + 1) * (S + 1);
-    static constexpr int H = 0;                          // S columns x LD
-    static constexpr int CF = 0;                         // coef_{k,i}: row k at k(k-1)/2 (S(S+1)/2)
-    static constexpr int P = S * (S + 1) / 2;            // P_k: row k at k(k+1)/2, length k+1
-    static constexpr int HS = AREA;                      // packed upper Hessenberg: column c at c(c+3)/2
-    static constexpr int HSN = (S - 1) * (S + 2) / 2 + S;
-    // the series scratch (T, SS, E: live after the charpoly) and the loop-chain vector (U:
-    // live before the reduction) share the packed Hessenberg's region, which is live only
-    // between the two (shared memory limits this kernel's teams per SM)
-    static constexpr bool ALIAS = HSN >= 3 * (kDMax + 2) && HSN >= 2 * S;
-    static constexpr int T = ALIAS ? HS : HS + HSN;      // [kDMax+2] traces
+    static constexpr int HSN = (S - 1) * (S + 2) / 2 + S;  // packed upper-Hessenberg entries
+    // Region A holds, in turn (shared memory limits this kernel's teams per SM, so
+    // nothing is kept twice):
+    //   * the S x S subset matrix (column-major, stride LD) during the reduction;
+    //   * the packed upper-Hessenberg form, column c at c(c+3)/2, packed IN PLACE column by
+    //     column (column c's packed slot ends below column c's own source for S <= 52);
+    //   * in the charpoly, the coefficients coef_{k,i} in place of h(i-1, k-1), and P_k
+    //     (coefficients 0..k-1; P_k[k] = 1 is implicit) in the slot of column k-2, dead
+    //     once P_{k-1} is built (it has exactly k entries); the final P_S goes to A;
+    //   * after the charpoly, the monic charpoly A and the series scratch T, SS, E, beyond
+    //     the packed region.
+    // (S > 52: the packed form goes to its own region after the matrix)
+    static constexpr bool INPLACE = S <= 52;
+    static constexpr int H = 0;
+    static constexpr int HS = INPLACE ? 0 : S * LD;
+    static constexpr int A = HS + HSN;                   // [S+1] monic charpoly, ascending
+    static constexpr int T = A + S + 1;                  // [kDMax+2] traces
     static constexpr int SS = T + kDMax + 2;             // [kDMax+2] series
     static constexpr int E = SS + kDMax + 2;             // [kDMax+2] exp Horner state
-    static constexpr int U = ALIAS ? HS : E + kDMax + 2;  // [2][S] loop-chain vector
-    static constexpr int MU = ALIAS ? HS + HSN : U + 2 * S;  // [S+2] multipliers by logical row
+    static constexpr int AREA = S * LD > E + kDMax + 2 ? S * LD : E + kDMax + 2;
+    static constexpr int U = AREA;                       // [2][S] loop-chain vector (before the reduction)
+    static constexpr int MU = U + 2 * S;                 // [S+2] multipliers by logical row
     static constexpr int ELL = MU + S + 2;               // [kDMax+2] loop corrections
     static constexpr int RED = ELL + kDMax + 2;          // [8] cross-warp exchange (W = 64)
-    static constexpr int INTS = RED + 8;                 // int area (in cd slots)
+    static constexpr int P1 = RED + 8;                   // [1] P_1[0]
+    static constexpr int INTS = P1 + 2;                  // int area (in cd slots)
     static constexpr int LMN = (2 * S + 3 * (S + 2) + 3) / 4 + 1;  // lm[2][S], stop[S+2], misc
     static constexpr int TOTAL = INTS + LMN;
 };
@@ -126,7 +141,7 @@ __device__ __forceinline__ cd team_bcast(const TeamCtx<W>& tc, cd* red, cd v, in
 }
 
 template <int S, bool LOOPS>
-__global__ void __launch_bounds__(kMirrorThreads) mirror_term_kernel(
+__global__ void __launch_bounds__(kMirrorThreads, mirror_minb<S>()) mirror_term_kernel(
     const cd* __restrict__ atilde, const cd* __restrict__ diag, int n_half, ClassItems ci,
     cd* __restrict__ terms, int8_t* __restrict__ status) {
     constexpr int W = TeamWidth<S>::W;
@@ -146,8 +161,6 @@ __global__ void __launch_bounds__(kMirrorThreads) mirror_term_kernel(
     const int lane = tc.lane;
     cd* ws = smem + (size_t)tc.tib * L::TOTAL;
     cd* H = ws + L::H;
-    cd* CF = ws + L::CF;
-    cd* PT = ws + L::P;
     cd* MU = ws + L::MU;
     cd* T = ws + L::T;
     cd* SSr = ws + L::SS;
@@ -291,16 +304,26 @@ __global__ void __launch_bounds__(kMirrorThreads) mirror_term_kernel(
             tc.sync();
         }
         const int* lmf = LM0 + ((S - 2) & 1) * S;  // final logical row -> lane
-        // pack the reduced (upper Hessenberg) form: logical row i, columns c >= i-1
+        // pack the reduced (upper Hessenberg) form in place: logical row i, columns
+        // c >= i-1.  Column c's packed slot ends below its own source and overlaps only
+        // the sources of columns < c, which are read already (c(c+3)/2 + c + 2 <= c(S+1)
+        // for S <= 52; larger S pack into a separate region).
         cd* HSp = ws + L::HS;
-        if (lane < S) {
-            const int ph = lmf[lane];
-            for (int c = lane > 0 ? lane - 1 : 0; c < S; ++c) HSp[(c * (c + 3)) / 2 + lane] = H[c * LD + ph];
+#pragma unroll 1
+        for (int c = 0; c < S; ++c) {
+            const bool on = lane < S && lane <= c + 1;
+            const cd v = on ? H[c * LD + lmf[lane]] : mk(0.0, 0.0);
+            tc.sync();
+            if (on) HSp[(c * (c + 3)) / 2 + lane] = v;
         }
-        tc.sync();  // region A is reused by CF / P from here on
+        tc.sync();
         auto h = [&](int i, int c) -> cd { return HSp[(c * (c + 3)) / 2 + i]; };
+        // P_m[d] for d < m (m >= 1; slot of column m-2, P_1 in its own cell)
+        auto pslot = [&](int m) -> cd* { return m >= 2 ? HSp + ((m - 2) * (m + 1)) / 2 : ws + L::P1; };
+        cd* Af = ws + L::A;
         // ------------------------------------------------ charpoly (_numba.py:203-225)
-        // (1) coefficient chains: lane k-1 walks prod/coef of P_k, i = k-1 .. 1
+        // (1) coefficient chains: lane k-1 walks prod/coef of P_k, i = k-1 .. 1; coef_{k,i}
+        //     replaces h(i-1, k-1) (read only by this lane; the chains read subdiagonals)
         if (lane < S) {
             const int k = lane + 1;
             cd prod = mk(1.0, 0.0);
@@ -308,40 +331,46 @@ __global__ void __launch_bounds__(kMirrorThreads) mirror_term_kernel(
             for (int i = k - 1; i > 0; --i) {
                 prod = m_mul(prod, h(i, i - 1));
                 if (!m_nz(prod)) break;
-                CF[(k * (k - 1)) / 2 + i] = m_mul(h(i - 1, k - 1), prod);
+                cd* cp = HSp + ((k - 1) * (k + 2)) / 2 + (i - 1);
+                *cp = m_mul(*cp, prod);
                 stop = i;
             }
             STOP[k] = stop;
         }
-        if (lane == 0) PT[0] = mk(1.0, 0.0);
         tc.sync();
         // (2) P_k over k; lane d owns coefficient d
         for (int k = 1; k <= S; ++k) {
             const cd hk = h(k - 1, k - 1);
-            const cd* Pk1 = PT + ((k - 1) * k) / 2;
-            cd* Pk = PT + (k * (k + 1)) / 2;
+            const cd* Pk1 = pslot(k >= 2 ? k - 1 : 1);  // P_{k-1}[d], d < k-1 (unused for k = 1)
+            cd* Pk = k < S ? pslot(k) : Af;
             const int stop = STOP[k];
+            const cd* coefs = HSp + ((k - 1) * (k + 2)) / 2;  // coef_{k,i} at i-1
             for (int d = lane; d <= k; d += W) {
+                // P_{k-1}[e] with the implicit leading 1 (P_0 = 1)
+                auto pk1 = [&](int e) -> cd { return e == k - 1 ? mk(1.0, 0.0) : Pk1[e]; };
                 cd v;
                 if (d == k) {
-                    v = Pk1[k - 1];
+                    v = mk(1.0, 0.0);  // P_{k-1}[k-1]
                 } else {
-                    const cd base0 = d >= 1 ? Pk1[d - 1] : mk(0.0, 0.0);
-                    v = m_sub(base0, m_mul(hk, Pk1[d]));
+                    const cd base0 = d >= 1 ? pk1(d - 1) : mk(0.0, 0.0);
+                    v = m_sub(base0, m_mul(hk, pk1(d)));
                 }
 #pragma unroll kMirrorCpUnroll
                 for (int i = k - 1; i >= stop && i > 0; --i) {
-                    const cd coef = CF[(k * (k - 1)) / 2 + i];
+                    const cd coef = coefs[i - 1];
                     // every lane computes, d < i selects (no divergent region; the read for
-                    // d >= i lands on a finite neighbouring table entry and is discarded)
-                    const cd t = m_sub(v, m_mul(coef, PT[((i - 1) * i) / 2 + d]));
+                    // d >= i - 1 is replaced by the implicit 1 or lands on a finite entry of
+                    // the shared table and is discarded)
+                    const cd* pim = pslot(i >= 2 ? i - 1 : 1);  // (P_0: only the implicit 1 is used)
+                    const cd pv = d == i - 1 ? mk(1.0, 0.0) : pim[d < i ? d : 0];
+                    const cd t = m_sub(v, m_mul(coef, pv));
                     if (m_nz(coef) && d < i) v = t;
                 }
-                Pk[d] = v;
+                if (k == S || d < k) Pk[d] = v;
             }
             tc.sync();
         }
-        const cd* a = PT + (S * (S + 1)) / 2;  // monic charpoly, ascending, a[S] = 1
+        const cd* a = Af;  // monic charpoly, ascending, a[S] = 1
         // ------------------------------------------------ Newton + Cayley-Hamilton (_numba.py:228-250)
         // sequential; every lane replays it (lane 0 stores)
         int bad = 0;

@@ -23,6 +23,10 @@ namespace hafb {
 #define HAFB_SMEM_HI 34
 #endif
 constexpr bool smem_hess(int S) { return !ns_variant(S) && ((S >= 18 && S <= 24) || S >= HAFB_SMEM_HI); }
+// the FAST spectral backend runs where the kernel keeps the packed Hessenberg form
+constexpr bool fast_spectral_ok(int S, bool loops) {
+    return (nsx_variant(S) && !loops) || !smem_hess(S);
+}
 
 // Threads per block.  The register classes run ONE block per SM whose teams are
 // phase-synchronised (__syncthreads between the Hessenberg, charpoly and series phases):
@@ -52,9 +56,9 @@ constexpr int threads_for(int S) {
 #define HAFB_NSX_THREADS 256
 #endif
 
-template <int S, bool L>
+template <int S, bool L, bool SPEC = false>
 static cudaError_t launch_one(const cd* at, const cd* dg, int n_half, const ClassItems& ci,
-                              cd* terms, int8_t* status, cudaStream_t st, int sms) {
+                              cd* terms, int8_t* status, cudaStream_t st, int sms, int cap = 0) {
     // S = 34, 36 without loops: one-warp teams with the extra rows held column-wise
     constexpr bool NSX = nsx_variant(S) && !L;
     constexpr bool SH = smem_hess(S) && !NSX;
@@ -68,7 +72,7 @@ static cudaError_t launch_one(const cd* at, const cd* dg, int n_half, const Clas
     const int optin = device_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin);
     const int stage = (NT > kFastThreads && !SH && base_smem + a_bytes <= (size_t)optin) ? 1 : 0;
     const size_t smem = base_smem + (stage ? a_bytes : 0);
-    auto kern = fast_term_kernel<S, L, SH, NT>;
+    auto kern = fast_term_kernel<S, L, SH, NT, SPEC>;
     // smem depends on n (the staged Atilde): the attribute is the size-independent
     // opt-in maximum, so host threads launching different n never race on it
     int occ = 1;
@@ -77,14 +81,25 @@ static cudaError_t launch_one(const cd* at, const cd* dg, int n_half, const Clas
     const long long want = (ci.n_items + TPB - 1) / TPB;
     const long long cap_blocks = (long long)sms * std::max(occ, 1);
     const int grid = (int)std::max<long long>(1, std::min(want, cap_blocks));
-    kern<<<grid, NT, smem, st>>>(at, dg, n_half, ci, terms, status, stage);
+    kern<<<grid, NT, smem, st>>>(at, dg, n_half, ci, terms, status, stage, cap);
     return cudaGetLastError();
 }
 
 template <>
 cudaError_t launch_fast_S<HAFB_S>(bool loops, const cd* at, const cd* dg, int n_half,
                                   const ClassItems& ci, cd* terms, int8_t* status, cudaStream_t st,
-                                  int sms) {
+                                  int sms, bool spectral, int cap) {
+    if (spectral) {
+        // the FAST spectral backend needs the packed Hessenberg form (not the 64-lane
+        // shared-memory classes: the caller routes those to the bit-exact kernel)
+        if constexpr (fast_spectral_ok(HAFB_S, true)) {
+            if (loops) return launch_one<HAFB_S, true, true>(at, dg, n_half, ci, terms, status, st, sms, cap);
+        }
+        if constexpr (fast_spectral_ok(HAFB_S, false)) {
+            if (!loops) return launch_one<HAFB_S, false, true>(at, dg, n_half, ci, terms, status, st, sms, cap);
+        }
+        return cudaErrorNotSupported;  // the caller runs the bit-exact spectral kernel
+    }
     return loops ? launch_one<HAFB_S, true>(at, dg, n_half, ci, terms, status, st, sms)
                  : launch_one<HAFB_S, false>(at, dg, n_half, ci, terms, status, st, sms);
 }

@@ -79,10 +79,13 @@ inline int device_attr(cudaDeviceAttr a) {
 
 constexpr int kFastSMax = 48;  // sizes above run in the shared-memory kernel
 
-// launch fast_term_kernel<S, loops> over the items of one popcount class
+// launch fast_term_kernel<S, loops> over the items of one popcount class; spectral: the
+// FAST spectral backend (QR on the Hessenberg form, sweeps capped at cap * S) --
+// fast_spectral_ok(S, loops) says where it exists
 template <int S>
 cudaError_t launch_fast_S(bool loops, const cd* at, const cd* dg, int n_half, const ClassItems& ci,
-                          cd* terms, int8_t* status, cudaStream_t st, int sms);
+                          cd* terms, int8_t* status, cudaStream_t st, int sms, bool spectral = false,
+                          int cap = 0);
 
 // launch mirror_term_kernel<S, loops> (bit-exact charpoly backend), S = 2..62
 template <int S>

@@ -274,6 +274,24 @@ cudaError_t launch_fast_class(int S, const cd* at, const cd* dg, int n_half, con
     }
 }
 
+// FAST spectral backend for one class; cudaErrorNotSupported where the FAST kernel does
+// not keep the packed Hessenberg form (then the bit-exact spectral kernel runs)
+template <bool L>
+cudaError_t launch_fast_spectral_class(int S, const cd* at, const cd* dg, int n_half,
+                                       const ClassItems& ci, int cap, cd* terms, int8_t* status,
+                                       cudaStream_t st) {
+    const int sms = sm_count();
+    switch (S) {
+#define FS(SS) \
+    case SS: return launch_fast_S<SS>(L, at, dg, n_half, ci, terms, status, st, sms, true, cap);
+        FS(2) FS(4) FS(6) FS(8) FS(10) FS(12) FS(14) FS(16) FS(18) FS(20) FS(22) FS(24)
+        FS(26) FS(28) FS(30) FS(32) FS(34) FS(36) FS(38) FS(40) FS(42) FS(44) FS(46) FS(48)
+#undef FS
+        default:
+            return cudaErrorNotSupported;
+    }
+}
+
 template <bool L>
 cudaError_t launch_mirror_class(int S, const cd* at, const cd* dg, int n_half,
                                 const ClassItems& ci, cd* terms, int8_t* status, cudaStream_t st) {
@@ -294,9 +312,17 @@ cudaError_t launch_mirror_class(int S, const cd* at, const cd* dg, int n_half,
 cudaError_t launch_class(int backend, int arith, bool loops, int S, const cd* at, const cd* dg,
                          int n_half, const ClassItems& ci, int cap, cd* terms, int8_t* status,
                          cudaStream_t st) {
-    if (backend == 0)  // spectral: shared-memory kernel (MIRROR arithmetic), one class per launch
+    if (backend == 0) {
+        // spectral: FAST = QR on the FAST kernel's packed Hessenberg form where it has one;
+        // MIRROR (and the remaining FAST sizes) = the bit-exact shared-memory kernel
+        if (arith == HAFB_ARITH_FAST) {
+            const cudaError_t e = loops ? launch_fast_spectral_class<true>(S, at, dg, n_half, ci, cap, terms, status, st)
+                                        : launch_fast_spectral_class<false>(S, at, dg, n_half, ci, cap, terms, status, st);
+            if (e != cudaErrorNotSupported) return e;
+        }
         return loops ? launch_smem_class<true, 0>(at, dg, n_half, ci, cap, terms, status, st)
                      : launch_smem_class<false, 0>(at, dg, n_half, ci, cap, terms, status, st);
+    }
     if (arith == HAFB_ARITH_MIRROR)
         return loops ? launch_mirror_class<true>(S, at, dg, n_half, ci, terms, status, st)
                      : launch_mirror_class<false>(S, at, dg, n_half, ci, terms, status, st);

@@ -1041,6 +1041,7 @@ __device__ __forceinline__ void nsx_hessenberg(cd (&w)[S], cd (&ex)[S - 32], int
 // team width of the FAST kernel: NSX sizes (no loops) run one-warp teams
 }  // namespace hafb
 #include "charpoly_mma.cuh"
+#include "qr_fast.cuh"
 namespace hafb {
 
 template <int S, bool LOOPS, bool SH>
@@ -1049,13 +1050,16 @@ struct FastTeam {
     static constexpr int W = NSX ? 32 : TeamWidth<S>::W;
 };
 
-template <int S, bool LOOPS, bool SH, int NT = kFastThreads>
+// SPEC: the spectral backend (qr_fast.cuh: shifted QR on the same packed Hessenberg
+// form, power sums) instead of the charpoly; cap_mult bounds its sweeps
+template <int S, bool LOOPS, bool SH, int NT = kFastThreads, bool SPEC = false>
 __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ atilde,
                                                                  const cd* __restrict__ diag,
                                                                  int n_half, ClassItems ci,
                                                                  cd* __restrict__ terms,
                                                                  int8_t* __restrict__ status,
-                                                                 int stage_a) {
+                                                                 int stage_a, int cap_mult) {
+    static_assert(!SPEC || !SH, "the FAST spectral backend runs on the packed Hessenberg form");
     constexpr bool NSX = FastTeam<S, LOOPS, SH>::NSX;
     // blocks of more than 128 threads (one block per SM) keep their teams in the same phase
     // (one phase's code in the instruction cache at a time) where that measured faster:
@@ -1242,7 +1246,16 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
         // one-warp register classes: blocked, the old-polynomial part on the FP64 tensor
         // cores (charpoly_mma.cuh); otherwise lane d owns coefficient d of every P_k
         constexpr bool CPMMA = HAFB_CP_MMA && W == 32 && !SH && S >= 18 && S <= 40;
-        if constexpr (CPMMA) {
+        bool conv = true;
+        if constexpr (SPEC) {
+            // ------------------------------------------ eigenvalues + power sums
+            // (_numba.py:115-200): traces t_k straight into T[1..D]
+            cd* eig = ws + L::A;
+            int sweeps = 0;
+            conv = q_eigvals<S, W>(ws + L::HS, eig, cap_mult, lane, sweeps, [&] { tc.sync(); });
+            if (conv) q_power_sums<S, W>(eig, ws + L::T, D, lane);
+            tc.sync();
+        } else if constexpr (CPMMA) {
             charpoly_mma<S, L>(ws, lane);
         } else {
             const cd* Hs = ws + L::HS;
@@ -1359,7 +1372,7 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
         cd* A = ws + L::A;
         int bad = 0;
         cd eD = mk(0.0, 0.0);
-        constexpr bool QS = !LOOPS && W <= 32 && HAFB_QSERIES;
+        constexpr bool QS = !LOOPS && W <= 32 && HAFB_QSERIES && !SPEC;
         if constexpr (QS) {
             // Without loop weights the series is exp(sum_k t_k x^k / (2k)) = q(x)^(-1/2) with
             // q(x) = det(I - xB) = sum_j a_j x^j, a_j = A[S-j] (the reversed charpoly), so
@@ -1442,7 +1455,7 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
             if (lane == (D - 1) % W && (!isfinite(eD.re) || !isfinite(eD.im))) bad = 1;
             bad = __any_sync(tc.wmask, bad);
         } else {
-        {
+        if constexpr (!SPEC) {
             cd acck[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -1479,10 +1492,14 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
                 }
             }
             tc.sync();
+        }
+        {
             // g_k = k s_k = t_k / 2 (+ k ell_k / 2 with loops)
             for (int k = lane + 1; k <= D; k += W) {
                 cd tk = T[k];
-                if (!isfinite(tk.re) || !isfinite(tk.im)) bad = 1;
+                // non-finite traces: status 2 on the charpoly backend; the reference's
+                // spectral path has no such check (_numba.py:322-331)
+                if (!SPEC && (!isfinite(tk.re) || !isfinite(tk.im))) bad = 1;
                 cd g = mk(0.5 * tk.re, 0.5 * tk.im);
                 if constexpr (LOOPS) g = mk(fma(0.5 * k, G[k].re, g.re), fma(0.5 * k, G[k].im, g.im));
                 G[k] = g;
@@ -1552,8 +1569,10 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
         }
         if (valid && lane == ((D - 1) % W)) {
             const bool neg = ((D - M) & 1) != 0;
-            terms[ir.out] = bad ? mk(0.0, 0.0) : (neg ? mk(-eD.re, -eD.im) : eD);
-            if (bad) status[ir.out] = 2;  // the buffer is zeroed by the host (no scattered byte writes)
+            terms[ir.out] = (bad || !conv) ? mk(0.0, 0.0) : (neg ? mk(-eD.re, -eD.im) : eD);
+            // the buffer is zeroed by the host (no scattered byte writes)
+            if (bad) status[ir.out] = 2;
+            if (!conv) status[ir.out] = 1;  // eigensolver non-convergence (_numba.py:322-324)
         }
         tc.sync();
         HT_MARK(4);

@@ -9,8 +9,8 @@ module as ``hafnium/kernels/_b200.py`` (a one-line re-export) behind
 
 Arithmetic: ``HAFB200_ARITH`` (read per call; default "mirror") picks MIRROR
 (bit-identical to the numba kernels) or FAST (FMA-contracted, within the
-rounding-level bound of accuracy.py).  FAST applies to the charpoly backend;
-the spectral backend runs its bit-exact QR kernel in either mode.
+rounding-level bound of accuracy.py) for both backends: FAST spectral runs the
+reference's shifted QR in FMA arithmetic (csrc/qr_fast.cuh).
 """
 
 from __future__ import annotations

@@ -163,8 +163,9 @@ def test_more_devices_than_visible_is_a_clear_error(monkeypatch):
         engine.hafnian(workloads.cfg0(), backend="charpoly", devices=4)
 
 
-def test_fast_arith_requires_charpoly_backend():
-    with pytest.raises(ValueError, match="charpoly"):
-        engine.EngineOptions(backend="spectral", arith="fast").validate()
-    engine.EngineOptions(backend="charpoly", arith="fast").validate()
-    engine.EngineOptions(backend="spectral", arith="mirror").validate()
+def test_arith_backend_combinations_validate():
+    for backend in ("spectral", "charpoly"):
+        for arith in ("fast", "mirror"):
+            engine.EngineOptions(backend=backend, arith=arith).validate()
+    with pytest.raises(ValueError, match="arith"):
+        engine.EngineOptions(arith="exact").validate()

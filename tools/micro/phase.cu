@@ -42,19 +42,22 @@ int main(int argc, char** argv) {
 #endif
     const int stage = (NTV > kFastThreads && !SHV) ? 1 : 0;
     size_t smem = (size_t)TPB * FastLayout<HAFB_S, SHV, false>::TOTAL * sizeof(cd) + kInvSlots * 8 + (stage ? (size_t)n * (n + 1) * sizeof(cd) : 0);
-    auto k = fast_term_kernel<HAFB_S, false, SHV, NTV>;
+    #ifndef SPECV
+#define SPECV false
+#endif
+    auto k = fast_term_kernel<HAFB_S, false, SHV, NTV, SPECV>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int occ; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NTV, smem);
     int grid = 148 * occ;
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-    k<<<grid, NTV, smem>>>(d_at, d_dg, D, ci, d_t, d_s, stage);
+    k<<<grid, NTV, smem>>>(d_at, d_dg, D, ci, d_t, d_s, stage, 30);
     cudaDeviceSynchronize();
 #ifdef HAFB_TIMING
     unsigned long long z[16] = {0};
     cudaMemcpyToSymbol(g_phase, z, sizeof(z)); cudaMemcpyToSymbol(g_phase_cnt, z, sizeof(z));
 #endif
     cudaEventRecord(e0);
-    k<<<grid, NTV, smem>>>(d_at, d_dg, D, ci, d_t, d_s, stage);
+    k<<<grid, NTV, smem>>>(d_at, d_dg, D, ci, d_t, d_s, stage, 30);
     cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     unsigned long long ph[16] = {0}, pc[16] = {0};

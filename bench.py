@@ -19,6 +19,9 @@ fixed as N grows ("scaling": "strong").  Rank 0 prints ONE JSON line.
   configs     every BASELINE config (cfg0..cfg4 incl. the 4096-matrix batch, the loop
               hafnian, n=56 and seed 4): terms/s, s/hafnian, roofline fractions, accuracy
               against the extended-precision referee, and the reference's CPU time
+  spectral    the reference's default backend (spectral: Hessenberg + shifted QR) on the
+              identical range [0, 2^20): FAST spectral, bit-exact MIRROR spectral (checked
+              against the C oracle), the unmodified reference and the C port on host cores
   cpu_baseline  the UNMODIFIED reference (hafnium 0.1.0 numba kernels, installed in
               baseline/_ref) on all host cores, on a seeded uniform sample of the same
               workload's masks; the C port of it (oracle/) beside it
@@ -65,6 +68,8 @@ def parse(argv=None):
     ap.add_argument("--n", type=int, default=N_DEFAULT)
     ap.add_argument("--seed", type=int, default=SEED_DEFAULT)
     ap.add_argument("--arith", choices=["fast", "mirror"], default="fast")
+    ap.add_argument("--spectral-bits", type=int, default=20,
+                    help="spectral-backend leg on masks [0, 2^bits) (0 = skip)")
     ap.add_argument("--cpu-seconds", type=float, default=8.0,
                     help="CPU budget of the headline cpu_baseline sample")
     ap.add_argument("--ref-step-seconds", type=float, default=1.0,
@@ -174,6 +179,60 @@ def port_rate(at, dg, nh, seconds, threads, seed=7, loops=False):
     O.terms(at, dg, nh, masks, backend=1, include_loops=loops, threads=threads)
     dt = time.perf_counter() - t0
     return count / dt, count, dt
+
+
+def run_spectral(at, dg, nh, device, args, cref, threads, ref_cache):
+    """backend='spectral' (the reference's default) on masks [0, 2^bits) of the workload:
+    FAST and MIRROR through the range ABI (host inputs, partials back; best of 2 after a
+    warm-up), the reference (numba) and the C port on a uniform sample of the same range,
+    MIRROR checked bit for bit against the C oracle and FAST against the referee."""
+    from oracle import oracle as O
+    from paper_1805_12498_b200 import engine, kernels
+
+    bits = min(args.spectral_bits, nh)
+    hi = 1 << bits
+    nterms = hi - 1
+    out = {"range": f"masks [0, 2^{bits}) of the n={args.n} workload (seed {args.seed}), 512 Kahan "
+                    f"chunks + fixed tree", "terms": nterms}
+    res = {}
+    for arith in ("fast", "mirror"):
+        kernels.sum_mask_range(at, dg, nh, 0, min(hi, 1 << 12), 512, 0, False, arith=arith, device=device)
+        ts = []
+        for _ in range(2):
+            t0 = time.perf_counter()
+            sums, fails = kernels.sum_mask_range(at, dg, nh, 0, hi, 512, 0, False, arith=arith, device=device)
+            ts.append(time.perf_counter() - t0)
+        r = engine.tree_reduce(sums)
+        res[arith] = r
+        out[arith] = {"value": nterms / min(ts), "unit": UNIT, "sec": min(ts), "result": [r.real, r.imag],
+                      "fails": int(fails.max())}
+    O.build()
+    r_orc = O.tree_reduce(O.sum_mask_range(at, dg, nh, 0, hi, 512, 0, False)[0])
+    out["mirror"]["bit_identical_to_oracle"] = bool(res["mirror"] == r_orc)
+    key = f"range_n{args.n}s{args.seed}"
+    if bits == 20 and key in ref_cache:
+        out["fast"]["accuracy"] = _score(res["fast"], ref_cache, key)
+        out["mirror"]["accuracy"] = _score(res["mirror"], ref_cache, key)
+    rng = np.random.default_rng(11)
+    masks = rng.integers(1, hi, 20000, dtype=np.uint64)
+    t0 = time.perf_counter()
+    O.terms(at, dg, nh, masks, backend=0, threads=threads)
+    dt = time.perf_counter() - t0
+    out["cpu_port"] = {"value": masks.size / dt, "unit": UNIT, "cores": threads, "kind": "port",
+                       "sample": f"{masks.size} uniform masks of the range ({dt:.2f} s), oracle/"
+                                 f"hafnian_oracle.c spectral"}
+    if cref is not None:
+        cref.terms(at, dg, nh, masks[:64].astype(np.int64), 0)  # JIT
+        t0 = time.perf_counter()
+        cref.terms(at, dg, nh, masks.astype(np.int64), 0)
+        dt = time.perf_counter() - t0
+        out["cpu_reference"] = {"value": masks.size / dt, "unit": UNIT, "cores": threads,
+                                "kind": "reference",
+                                "sample": f"{masks.size} uniform masks of the range ({dt:.2f} s), the "
+                                          f"unmodified reference (numba, backend=0)"}
+        out["speedup_fast_vs_reference"] = out["fast"]["value"] / out["cpu_reference"]["value"]
+    out["speedup_fast_vs_port"] = out["fast"]["value"] / out["cpu_port"]["value"]
+    return out
 
 
 def cpu_model() -> str:
@@ -725,6 +784,13 @@ def run_ours(args):
                       "sec": t3, "result": str(cnt3),
                       "matches_known_answer": cnt3 == 308544357990268074}
 
+    # the reference's DEFAULT backend (spectral: Hessenberg + shifted QR) on the identical
+    # range [0, 2^20) of this workload: FAST spectral, bit-exact MIRROR spectral, and the
+    # unmodified reference / the C port on the host cores
+    spectral = None
+    if rank == 0 and world == 1 and args.spectral_bits > 0:
+        spectral = run_spectral(at, dg, nh, local, args, cref, threads, ref_cache)
+
     # per-config legs and the multi-GPU proxy (one GPU, rank 0 of a single-rank run)
     configs = proxy = None
     if rank == 0 and world == 1 and not args.no_configs:
@@ -841,7 +907,7 @@ def run_ours(args):
             "gpu_launches": launches,
             "clocks": clk,
         }
-        for k, v in (("mirror", mirror), ("exact", exact_line), ("configs", configs),
+        for k, v in (("mirror", mirror), ("spectral", spectral), ("exact", exact_line), ("configs", configs),
                      ("multi_gpu_proxy", proxy), ("parity", parity), ("cpu_baseline", cpu)):
             if v is not None:
                 line[k] = v

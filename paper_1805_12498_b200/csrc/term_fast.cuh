@@ -1065,7 +1065,10 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
     // (one phase's code in the instruction cache at a time) where that measured faster:
     // the NSX classes (S = 34, 36: -15 %); the static-column classes S <= 32 run 2-3 %
     // faster without the phase barriers
-    constexpr bool PSYNC = NT > kFastThreads && (NSX || (HAFB_PSYNC && !ns_variant(S)));
+    #ifndef HAFB_PSYNC_NS
+#define HAFB_PSYNC_NS 0
+#endif
+    constexpr bool PSYNC = NT > kFastThreads && (NSX || (HAFB_PSYNC && (!ns_variant(S) || HAFB_PSYNC_NS)));
     constexpr int W = FastTeam<S, LOOPS, SH>::W;
     constexpr int TPB = NT / W;
     constexpr int M = S / 2;

@@ -246,7 +246,8 @@ ClassTables build_tables(int D, const std::vector<Seg>& segs) {
 template <bool L, int B = 1>
 cudaError_t launch_smem_class(const cd* at, const cd* dg, int n_half, const ClassItems& ci, int cap,
                               cd* terms, int8_t* status, cudaStream_t st) {
-    size_t per_warp = (size_t)smem_warp_elems(2 * ci.m, n_half) * sizeof(cd);
+    size_t per_warp = (size_t)(B == 0 ? smem_warp_elems_spec(2 * ci.m, n_half)
+                                      : smem_warp_elems(2 * ci.m, n_half)) * sizeof(cd);
     int wpb = (int)std::min<size_t>(8, std::max<size_t>(1, (200 * 1024) / per_warp));
     size_t smem = wpb * per_warp;
     auto kern = terms_smem_class_kernel<B, L>;

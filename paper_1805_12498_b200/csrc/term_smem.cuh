@@ -36,6 +36,12 @@ __host__ __device__ inline int smem_warp_elems(int S, int K) {
     return hreg + pt + 6 * (S + 2) + 3 * (K + 2);
 }
 __host__ __device__ inline int smem_warp_elems(int n) { return smem_warp_elems(n, n / 2); }
+// the spectral class kernel's compact workspace: the S x S matrix, five S+2 vectors
+// (loop vectors, the vertex list, eigenvalues) and three K+2 series vectors -- no
+// charpoly table, and the power sums need no S x K scratch (lane k recomputes the
+// reference's power chain, see subset_term_smem).  At S = 20, n = 52: 9.5 KB per warp
+// instead of 15.5 KB, two 8-warp blocks per SM instead of one.
+__host__ __device__ inline int smem_warp_elems_spec(int S, int K) { return S * S + 5 * (S + 2) + 3 * (K + 2); }
 
 struct WarpWs {
     cd* H;    // s*s, row-major, ld = s (also the s*K power-sum scratch)
@@ -71,6 +77,23 @@ __device__ inline WarpWs carve(cd* base, int S, int K) {
     return w;
 }
 __device__ inline WarpWs carve(cd* base, int n) { return carve(base, n, n / 2); }
+__device__ inline WarpWs carve_spec(cd* base, int S, int K) {
+    WarpWs w;
+    w.H = base;
+    w.P = nullptr;
+    cd* q = w.H + S * S;
+    w.mu = nullptr;
+    w.v = q; q += S + 2;
+    w.xv = q; q += S + 2;
+    w.u = q; q += S + 2;
+    w.unew = q; q += S + 2;
+    w.eig = q; q += S + 2;
+    w.t = q; q += K + 2;
+    w.s = q; q += K + 2;
+    w.E = q; q += K + 2;
+    w.vec = nullptr;
+    return w;
+}
 
 // ------------------------------------------------------------------ Hessenberg
 // _numba.py:36-67.  The i-loop is sequential (each i's row op then column op);
@@ -345,20 +368,19 @@ __device__ inline void subset_term_smem(const cd* __restrict__ atilde, const cd*
         if (!conv) {
             status = 1;
         } else {
-            // _power_sums (_numba.py:191-200): t[k] accumulates eigenvalue i in order i.
-            // Lane i builds the power sequence of eig[i] into H rows (H is dead now).
-            __syncwarp();
-            for (int i = lane; i < size; i += 32) {
-                cd lam = w.eig[i], p = lam;
-                for (int k = 0; k < K; ++k) {
-                    w.H[i * K + k] = p;
-                    p = m_mul(p, lam);
-                }
-            }
+            // _power_sums (_numba.py:191-200): t[k] += p over eigenvalues i in order, with
+            // p = lam^(k+1) from the reference's chain p = lam, p *= lam, ...  Lane k replays
+            // that chain for its own k (the same k multiplications per eigenvalue, so the
+            // same bits) and accumulates over i in order: no S x K scratch.
             __syncwarp();
             for (int k = lane; k < K; k += 32) {
                 cd acc = mk(0.0, 0.0);
-                for (int i = 0; i < size; ++i) acc = m_add(acc, w.H[i * K + k]);
+                for (int i = 0; i < size; ++i) {
+                    const cd lam = w.eig[i];
+                    cd p = lam;
+                    for (int j = 0; j < k; ++j) p = m_mul(p, lam);
+                    acc = m_add(acc, p);
+                }
                 w.t[k] = acc;
             }
         }
@@ -495,7 +517,8 @@ __global__ void __launch_bounds__(256) terms_smem_class_kernel(
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     const int S = 2 * ci.m;  // one class per launch: size the workspace for it
-    WarpWs w = carve(smem + (size_t)wib * smem_warp_elems(S, n_half), S, n_half);
+    WarpWs w = BACKEND == 0 ? carve_spec(smem + (size_t)wib * smem_warp_elems_spec(S, n_half), S, n_half)
+                            : carve(smem + (size_t)wib * smem_warp_elems(S, n_half), S, n_half);
     const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
     for (long long it = (long long)blockIdx.x * (blockDim.x >> 5) + wib; it < ci.n_items; it += nwarps) {
         const ItemRef ir = resolve_item(ci, it);

@@ -230,10 +230,10 @@ __device__ inline void qr_sweep_smem(cd* H, int m, int lo, int hi, cd shift, int
         for (int col = col0 + lane; col <= hi; col += 32) {
             cd t1 = HH(k, col), t2 = HH(k + 1, col);
             HH(k, col) = m_add(m_rmul(c, t1), m_mul(s, t2));
-            HH(k + 1, col) = m_add(m_mul(m_neg(sc), t1), m_rmul(c, t2));
+            // col == k-1 (k > lo): the reference rotates, then sets h[k+1, k-1] = 0
+            // (_numba.py:102-103) -- store the final 0 directly
+            HH(k + 1, col) = col == k - 1 ? mk(0.0, 0.0) : m_add(m_mul(m_neg(sc), t1), m_rmul(c, t2));
         }
-        __syncwarp();
-        if (k > lo && lane == 0) HH(k + 1, k - 1) = mk(0.0, 0.0);
         __syncwarp();
         int row_end = k + 2;
         if (row_end > hi) row_end = hi;
@@ -264,16 +264,28 @@ __device__ inline bool hess_eigvals_smem(cd* H, int m, int cap_mult, cd* eig, in
             if (lane == 0) eig[0] = HH(0, 0);
             break;
         }
-        int lo = hi;
-        while (lo > 0) {
-            double sd = m_abs(HH(lo, lo - 1));
-            if (sd <= r_mul(kDeflationRtol, r_add(m_abs(HH(lo, lo)), m_abs(HH(lo - 1, lo - 1))))) {
-                __syncwarp();
-                if (lane == 0) HH(lo, lo - 1) = mk(0.0, 0.0);
-                __syncwarp();
+        // deflation scan (_numba.py:132-138): positions lo = hi, hi-1, ..., 1, the first
+        // small subdiagonal from the bottom wins.  Each lane evaluates the reference's test
+        // for one position (the same operations, so the same decisions) and a ballot picks
+        // the first hit: one round of three hypots instead of up to hi sequential ones.
+        int lo = 0;
+        for (int base = hi; base >= 1; base -= 32) {
+            const int p = base - lane;
+            bool small = false;
+            if (p >= 1) {
+                const double sd = m_abs(HH(p, p - 1));
+                small = sd <= r_mul(kDeflationRtol, r_add(m_abs(HH(p, p)), m_abs(HH(p - 1, p - 1))));
+            }
+            const unsigned b = __ballot_sync(0xffffffffu, small);
+            if (b) {
+                lo = base - (__ffs(b) - 1);
                 break;
             }
-            lo -= 1;
+        }
+        if (lo > 0) {
+            __syncwarp();
+            if (lane == 0) HH(lo, lo - 1) = mk(0.0, 0.0);
+            __syncwarp();
         }
         if (lo == hi) {
             if (lane == 0) eig[hi] = HH(hi, hi);

@@ -10,6 +10,14 @@ void shim_div(const double* a, const double* b, double* out) {
     out[0] = r.re;
     out[1] = r.im;
 }
+void shim_rdiv(const double* a, double r, double* out, double* ref) {
+    cd x = m_rdiv(mk(a[0], a[1]), r);
+    cd y = m_div(mk(a[0], a[1]), mk(r, 0.0));
+    out[0] = x.re;
+    out[1] = x.im;
+    ref[0] = y.re;
+    ref[1] = y.im;
+}
 void shim_sqrt(const double* a, double* out) {
     cd r = m_sqrt(mk(a[0], a[1]));
     out[0] = r.re;

@@ -25,6 +25,7 @@ def shim(tmp_path_factory):
     dp = ctypes.POINTER(ctypes.c_double)
     lib.shim_div.argtypes = [dp, dp, dp]
     lib.shim_sqrt.argtypes = [dp, dp]
+    lib.shim_rdiv.argtypes = [dp, ctypes.c_double, dp, dp]
     return lib
 
 
@@ -75,3 +76,23 @@ def test_sqrt_matches_numpy_csqrt_for_finite(shim):
         r = complex(out[0], out[1])
         worst = max(worst, abs(r - cmath.sqrt(z)) / abs(cmath.sqrt(z)))
     assert worst < 4e-16
+
+
+def test_rdiv_is_div_by_real_bit_for_bit(shim):
+    """m_rdiv (complex / real, the ratio and denominator folded) returns exactly the bits
+    of the general Smith division by (r, 0), special values and signed zeros included."""
+    rng = np.random.default_rng(10)
+    vals = [0.0, -0.0, 1.0, -1.0, np.inf, -np.inf, np.nan, 5e-324, -5e-324, 1e308, -1e-308]
+    A = [complex(a, b) for a in vals for b in vals]
+    A += [complex(*rng.normal(size=2) * 10.0 ** rng.integers(-300, 300, 2)) for _ in range(20000)]
+    R = vals + list(rng.normal(size=2000) * 10.0 ** rng.integers(-300, 300, 2000))
+    out, ref = (ctypes.c_double * 2)(), (ctypes.c_double * 2)()
+    bad = 0
+    for i, a in enumerate(A):
+        for r in (R[i % len(R)], R[(7 * i + 3) % len(R)]):
+            shim.shim_rdiv(_c(a), r, out, ref)
+            got = np.array([out[0], out[1]]).view(np.uint64)
+            exp = np.array([ref[0], ref[1]]).view(np.uint64)
+            same = (got == exp) | (np.isnan([out[0], out[1]]) & np.isnan([ref[0], ref[1]]))
+            bad += int(not same.all())
+    assert bad == 0

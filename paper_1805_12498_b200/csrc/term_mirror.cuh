@@ -196,6 +196,7 @@ __global__ void __launch_bounds__(kMirrorThreads, mirror_minb<S>()) mirror_term_
         }
         const int mybit = lane < S ? (int)__fns(ir.mask, 0, (lane >> 1) + 1) : 0;
         const int vr = 2 * mybit + (lane & 1);
+        HT_DECL
         // ------------------------------------------------ gather b = Atilde[idx][:, idx]
         if (lane < S) {
 #pragma unroll
@@ -227,6 +228,7 @@ __global__ void __launch_bounds__(kMirrorThreads, mirror_minb<S>()) mirror_term_
                 tc.sync();
             }
         }
+        HT_MARK(0);
         // ------------------------------------------------ Hessenberg (_numba.py:36-67)
         int myrow = lane;
         if (lane < S) LM0[lane] = lane;
@@ -321,6 +323,7 @@ __global__ void __launch_bounds__(kMirrorThreads, mirror_minb<S>()) mirror_term_
         // P_m[d] for d < m (m >= 1; slot of column m-2, P_1 in its own cell)
         auto pslot = [&](int m) -> cd* { return m >= 2 ? HSp + ((m - 2) * (m + 1)) / 2 : ws + L::P1; };
         cd* Af = ws + L::A;
+        HT_MARK(1);
         // ------------------------------------------------ charpoly (_numba.py:203-225)
         // (1) coefficient chains: lane k-1 walks prod/coef of P_k, i = k-1 .. 1; coef_{k,i}
         //     replaces h(i-1, k-1) (read only by this lane; the chains read subdiagonals)
@@ -371,6 +374,7 @@ __global__ void __launch_bounds__(kMirrorThreads, mirror_minb<S>()) mirror_term_
             tc.sync();
         }
         const cd* a = Af;  // monic charpoly, ascending, a[S] = 1
+        HT_MARK(2);
         // ------------------------------------------------ Newton + Cayley-Hamilton (_numba.py:228-250)
         // sequential; every lane replays it (lane 0 stores)
         int bad = 0;
@@ -402,6 +406,7 @@ __global__ void __launch_bounds__(kMirrorThreads, mirror_minb<S>()) mirror_term_
             E[k] = k == 0 ? mk(1.0, 0.0) : mk(0.0, 0.0);
         }
         tc.sync();
+        HT_MARK(3);
         // ------------------------------------------------ _exp_top (_numba.py:276-294), Horner
         for (int jj = D; jj > 0; --jj) {
             const double inv = r_div(1.0, (double)jj);
@@ -432,6 +437,7 @@ __global__ void __launch_bounds__(kMirrorThreads, mirror_minb<S>()) mirror_term_
             if (bad) status[ir.out] = 2;  // the buffer is zeroed by the host
         }
         tc.sync();
+        HT_MARK(4);
     }
 }
 

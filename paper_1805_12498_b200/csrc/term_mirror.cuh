@@ -87,7 +87,8 @@ struct MirrorLayout {
     static constexpr int P1 = RED + 8;                   // [1] P_1[0]
     static constexpr int INTS = P1 + 2;                  // int area (in cd slots)
     static constexpr int LMN = (2 * S + 3 * (S + 2) + 3) / 4 + 1;  // lm[2][S], stop[S+2], misc
-    static constexpr int TOTAL = INTS + LMN;
+    static constexpr int INVT = INTS + LMN;              // [kDMax+1] doubles: 1/j (_exp_top)
+    static constexpr int TOTAL = INVT + (kDMax + 2) / 2;
 };
 
 // first-strict-max argmax over (key, row): larger key wins, ties -> smaller row; NaN
@@ -178,6 +179,11 @@ __global__ void __launch_bounds__(kMirrorThreads, mirror_minb<S>()) mirror_term_
     const long long chunk = (ci.n_items + n_teams - 1) / n_teams;
     const long long first = ((long long)blockIdx.x * TPB + tc.tib) * chunk;
     ItemCursor cur;
+    // _exp_top's 1/j for every j: the same correctly rounded quotients, computed once per
+    // team instead of once per subset (D divisions on the chain of every term)
+    double* INVJ = reinterpret_cast<double*>(ws + L::INVT);
+    for (int j = lane; j <= kDMax; j += W) INVJ[j] = j ? r_div(1.0, (double)j) : 0.0;
+    tc.sync();
 
     for (long long it = 0; it < chunk; ++it) {
         const long long item = first + it;
@@ -409,7 +415,7 @@ __global__ void __launch_bounds__(kMirrorThreads, mirror_minb<S>()) mirror_term_
         HT_MARK(3);
         // ------------------------------------------------ _exp_top (_numba.py:276-294), Horner
         for (int jj = D; jj > 0; --jj) {
-            const double inv = r_div(1.0, (double)jj);
+            const double inv = INVJ[jj];  // = r_div(1.0, jj)
             cd f[(kDMax + W) / W];
 #pragma unroll
             for (int r = 0; r < (kDMax + W) / W; ++r) {

@@ -21,7 +21,12 @@
  *     different host threads are safe;
  *   - backend: 0 = spectral (Hessenberg + shifted QR), 1 = charpoly;
  *   - arith: 0 = MIRROR (the reference's exact IEEE operation sequence, results
- *     bit-identical to the reference), 1 = FAST (FMA-contracted kernels).
+ *     bit-identical to the reference), 1 = FAST (FMA-contracted kernels, results within
+ *     the rounding-level bound of paper_1805_12498_b200/accuracy.py) for both backends:
+ *     FAST charpoly = Hessenberg + tensor-core charpoly, FAST spectral = the same
+ *     Hessenberg + the reference's shifted QR in FMA arithmetic (status 1 on
+ *     non-convergence, as the reference); the entry points on a single matrix
+ *     (hafb_power_traces, hafb_charpoly_coefficients) run MIRROR.
  *
  * Sizes: n_half = n/2 in [1, 32] (masks are 32-bit on the device; n <= 64).
  */

@@ -35,6 +35,7 @@ struct ClassItems {
     const long long* mout;              // ... and their buffer indices (else null)
     Seg seg0;                           // nseg == 1: the segment and its base by value
     unsigned long long base0;           // (no dependent loads for the first item)
+    unsigned long long* ctr = nullptr;  // zeroed work counter: dynamic chunks (FAST kernels)
 };
 
 // the r-th (0-based) integer with popcount m, bits below D (combinatorial number

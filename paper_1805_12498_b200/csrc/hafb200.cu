@@ -341,6 +341,7 @@ struct DevTables {
     Seg* segs = nullptr;
     long long* prefix = nullptr;
     unsigned long long* base = nullptr;
+    unsigned long long* ctr = nullptr;  // [D+1] work counters (zero after upload)
     // the items of popcount class m (batch problems of `per` items each)
     ClassItems items(int m, int batch, long long term_stride, long long at_stride,
                      long long dg_stride) const {
@@ -362,6 +363,7 @@ struct DevTables {
         ci.term_stride = term_stride;
         ci.at_stride = at_stride;
         ci.dg_stride = dg_stride;
+        ci.ctr = ctr + m;
         return ci;
     }
 };
@@ -376,11 +378,13 @@ int upload_tables(int D, const std::vector<Seg>& segs, void* table_ws, cudaStrea
     dt.prefix = reinterpret_cast<long long*>(p);
     p += align256(sizeof(long long) * dt.t.prefix.size());
     dt.base = reinterpret_cast<unsigned long long*>(p);
+    p += align256(sizeof(unsigned long long) * (D + 1) * nseg);
+    dt.ctr = reinterpret_cast<unsigned long long*>(p);  // zeroed with the tables below
     // one host staging image of the four tables, one copy (a pageable copy costs
     // ~10 us each; small problems are launch- and copy-bound)
-    const size_t total = (size_t)(reinterpret_cast<char*>(dt.base) - static_cast<char*>(table_ws)) +
-                         sizeof(unsigned long long) * dt.t.base.size();
-    std::vector<char> img(total);
+    const size_t total = (size_t)(reinterpret_cast<char*>(dt.ctr) - static_cast<char*>(table_ws)) +
+                         sizeof(unsigned long long) * (D + 1);
+    std::vector<char> img(total, 0);  // (the counters travel as zeros)
     char* h = img.data();
     auto at_ = [&](const void* dptr) { return h + (static_cast<const char*>(dptr) - static_cast<char*>(table_ws)); };
     std::memcpy(at_(dt.segs), segs.data(), sizeof(Seg) * nseg);
@@ -479,7 +483,8 @@ cudaError_t launch_modp_class(int S, bool loops, const uint32_t* at, const uint3
 
 size_t table_ws_bytes(int n_half, size_t nseg) {
     return align256(sizeof(Seg) * nseg) + align256(sizeof(long long) * (n_half + 1) * (nseg + 1)) +
-           align256(sizeof(unsigned long long) * (n_half + 1) * nseg);
+           align256(sizeof(unsigned long long) * (n_half + 1) * nseg) +
+           align256(sizeof(unsigned long long) * (n_half + 1));  // per-class work counters
 }
 
 size_t mask_range_ws_bytes(int n_half, long long count) {

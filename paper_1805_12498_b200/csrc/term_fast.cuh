@@ -110,6 +110,9 @@ constexpr int kInvSlots = (kDMax + 2) & ~1;
 #ifndef HAFB_NS_HI
 #define HAFB_NS_HI 32
 #endif
+#ifndef HAFB_DYN_CHUNK
+#define HAFB_DYN_CHUNK 16
+#endif
 constexpr bool ns_variant(int S) { return HAFB_NS && S >= HAFB_NS_LO && S <= HAFB_NS_HI; }
 
 // packed upper-Hessenberg storage, column-major: column c holds rows 0..min(c+1, S-1)
@@ -1095,8 +1098,22 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
     // Gosper's step, ItemCursor); every team runs the same trip count (block-uniform
     // loop for the phase barriers)
     const long long n_teams = (long long)gridDim.x * TPB;
-    const long long chunk = (ci.n_items + n_teams - 1) / n_teams;
-    const long long first = ((long long)blockIdx.x * TPB + tc.tib) * chunk;
+    // Work distribution.  Static: team t walks items [t*chunk, (t+1)*chunk).  Dynamic
+    // (one problem, ci.ctr set): blocks take chunks of TPB*ch items from an atomic
+    // counter (ch items per team, walked contiguously), so the kernel's tail is one
+    // chunk rather than the spread of whole-kernel team times (measured ~5 ms per big
+    // class launch: 10 % of a 1/8 shard, 2-3 % of the full step).
+#ifndef HAFB_DYN
+#define HAFB_DYN 1
+#endif
+    const bool dyn = HAFB_DYN && ci.ctr != nullptr && ci.n_items == ci.per_problem;
+    long long ch = (ci.n_items + n_teams - 1) / n_teams;  // static: the whole run
+    if (dyn) {
+        ch = ci.n_items / (n_teams * 8);
+        ch = ch < 1 ? 1 : (ch > HAFB_DYN_CHUNK ? HAFB_DYN_CHUNK : ch);
+    }
+    const long long chunk = ch;
+    long long first = ((long long)blockIdx.x * TPB + tc.tib) * chunk;
     // Atilde staged in shared memory (row stride n+1: the lanes' rows fall in distinct
     // banks) for the block's first problem; the subset gathers then read shared memory
     // instead of issuing S scattered global loads per lane
@@ -1104,8 +1121,8 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
     const int ldA = n + 1;
     long long staged_problem = -1;
     const long long block_first = (long long)blockIdx.x * TPB * chunk;
-    if (stage_a && block_first < ci.n_items) {  // a block past the last item stages nothing
-        staged_problem = block_first / ci.per_problem;
+    if (stage_a && (dyn || block_first < ci.n_items)) {  // (static) a block past the last item stages nothing
+        staged_problem = dyn ? 0 : block_first / ci.per_problem;
         const cd* src = atilde + staged_problem * ci.at_stride;
         for (int i = threadIdx.x; i < n * n; i += blockDim.x) As[(i / n) * ldA + (i % n)] = src[i];
     }
@@ -1116,6 +1133,18 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
     __nanosleep((unsigned)(((threadIdx.x >> 5) + 4 * (blockIdx.x % 4)) % 16) * HAFB_STAGGER);
 #endif
 
+    // the dynamic chunk base travels through the spare slot of the 1/k table
+    long long* dyn_base = reinterpret_cast<long long*>(INV + (kInvSlots - 1));
+    for (;;) {
+    if (dyn) {
+        // block-uniform: every team of the block runs the same trip count (phase barriers)
+        __syncthreads();
+        if (threadIdx.x == 0) *dyn_base = (long long)atomicAdd(ci.ctr, (unsigned long long)(TPB * chunk));
+        __syncthreads();
+        const long long b0 = *dyn_base;
+        if (b0 >= ci.n_items) break;
+        first = b0 + (long long)tc.tib * chunk;
+    }
     for (long long it = 0; it < chunk; ++it) {
         HT_DECL
         const long long item = first + it;
@@ -1579,6 +1608,8 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
         }
         tc.sync();
         HT_MARK(4);
+    }
+    if (!dyn) break;
     }
 }
 

@@ -113,6 +113,9 @@ constexpr int kInvSlots = (kDMax + 2) & ~1;
 #ifndef HAFB_DYN_CHUNK
 #define HAFB_DYN_CHUNK 16
 #endif
+#ifndef HAFB_DYN_PER
+#define HAFB_DYN_PER 8
+#endif
 constexpr bool ns_variant(int S) { return HAFB_NS && S >= HAFB_NS_LO && S <= HAFB_NS_HI; }
 
 // packed upper-Hessenberg storage, column-major: column c holds rows 0..min(c+1, S-1)
@@ -1109,7 +1112,7 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
     const bool dyn = HAFB_DYN && ci.ctr != nullptr && ci.n_items == ci.per_problem;
     long long ch = (ci.n_items + n_teams - 1) / n_teams;  // static: the whole run
     if (dyn) {
-        ch = ci.n_items / (n_teams * 8);
+        ch = ci.n_items / (n_teams * HAFB_DYN_PER);  // >= HAFB_DYN_PER chunks per team
         ch = ch < 1 ? 1 : (ch > HAFB_DYN_CHUNK ? HAFB_DYN_CHUNK : ch);
     }
     const long long chunk = ch;

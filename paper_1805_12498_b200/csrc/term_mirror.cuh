@@ -176,8 +176,16 @@ __global__ void __launch_bounds__(kMirrorThreads, mirror_minb<S>()) mirror_term_
     // each team walks a contiguous run of the class's items (successive masks by Gosper's
     // step, ItemCursor): which team computes which subset changes, no arithmetic does
     const long long n_teams = (long long)gridDim.x * TPB;
-    const long long chunk = (ci.n_items + n_teams - 1) / n_teams;
-    const long long first = ((long long)blockIdx.x * TPB + tc.tib) * chunk;
+    // work distribution as in the FAST kernel: dynamic block chunks from the class's
+    // counter (every problem of a batch alike: this kernel stages nothing per block)
+    const bool dyn = HAFB_DYN && ci.ctr != nullptr;
+    long long ch = (ci.n_items + n_teams - 1) / n_teams;
+    if (dyn) {
+        ch = ci.n_items / (n_teams * HAFB_DYN_PER);
+        ch = ch < 1 ? 1 : (ch > HAFB_DYN_CHUNK ? HAFB_DYN_CHUNK : ch);
+    }
+    const long long chunk = ch;
+    long long first = ((long long)blockIdx.x * TPB + tc.tib) * chunk;
     ItemCursor cur;
     // _exp_top's 1/j for every j: the same correctly rounded quotients, computed once per
     // team instead of once per subset (D divisions on the chain of every term)
@@ -185,6 +193,17 @@ __global__ void __launch_bounds__(kMirrorThreads, mirror_minb<S>()) mirror_term_
     for (int j = lane; j <= kDMax; j += W) INVJ[j] = j ? r_div(1.0, (double)j) : 0.0;
     tc.sync();
 
+    // block-shared: the spare slot of team 0's 1/j table
+    long long* dyn_base = reinterpret_cast<long long*>(reinterpret_cast<double*>(smem + L::INVT) + kDMax + 1);
+    for (;;) {
+    if (dyn) {
+        __syncthreads();
+        if (threadIdx.x == 0) *dyn_base = (long long)atomicAdd(ci.ctr, (unsigned long long)(TPB * chunk));
+        __syncthreads();
+        const long long b0 = *dyn_base;
+        if (b0 >= ci.n_items) break;
+        first = b0 + (long long)tc.tib * chunk;
+    }
     for (long long it = 0; it < chunk; ++it) {
         const long long item = first + it;
         const bool valid = item < ci.n_items;
@@ -444,6 +463,8 @@ __global__ void __launch_bounds__(kMirrorThreads, mirror_minb<S>()) mirror_term_
         }
         tc.sync();
         HT_MARK(4);
+    }
+    if (!dyn) break;
     }
 }
 

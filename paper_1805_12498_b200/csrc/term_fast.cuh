@@ -1109,7 +1109,7 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
 #ifndef HAFB_DYN
 #define HAFB_DYN 1
 #endif
-    const bool dyn = HAFB_DYN && ci.ctr != nullptr && ci.n_items == ci.per_problem;
+    const bool dyn = HAFB_DYN && ci.ctr != nullptr;
     long long ch = (ci.n_items + n_teams - 1) / n_teams;  // static: the whole run
     if (dyn) {
         ch = ci.n_items / (n_teams * HAFB_DYN_PER);  // >= HAFB_DYN_PER chunks per team
@@ -1147,6 +1147,13 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
         const long long b0 = *dyn_base;
         if (b0 >= ci.n_items) break;
         first = b0 + (long long)tc.tib * chunk;
+        // a batch: re-stage Atilde when the block's chunk starts in another problem
+        if (stage_a && b0 / ci.per_problem != staged_problem) {
+            staged_problem = b0 / ci.per_problem;
+            const cd* src = atilde + staged_problem * ci.at_stride;
+            for (int i = threadIdx.x; i < n * n; i += blockDim.x) As[(i / n) * ldA + (i % n)] = src[i];
+            __syncthreads();
+        }
     }
     for (long long it = 0; it < chunk; ++it) {
         HT_DECL

@@ -1191,6 +1191,8 @@ int hafb_modp_sums(const uint32_t* atilde_p, const uint32_t* diag_p, const uint3
         CK(cudaEventRecord(e0, c.st));
     }
     for (int i = 0; i < n_primes; ++i) {
+        // each prime's class launches consume the per-class work counters afresh
+        if (i > 0) CK(cudaMemsetAsync(dt.ctr, 0, sizeof(unsigned long long) * (n_half + 1), c.st));
         for (int m = n_half; m >= 1; --m) {
             if (dt.t.count(m) == 0) continue;
             const ClassItems ci = dt.items(m, 1, 0, 0, 0);

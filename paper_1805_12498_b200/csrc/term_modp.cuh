@@ -196,12 +196,29 @@ __global__ void __launch_bounds__(kModpThreads) modp_term_kernel(
     const uint32_t p = M.p;
     const uint32_t inv2 = tab[2];
     unsigned long long my_sum = 0;  // lane 0: this team's terms (each < p)
-    // contiguous per-team runs of the class's items (Gosper's step, ItemCursor)
+    // contiguous per-team runs of the class's items (Gosper's step, ItemCursor), in
+    // dynamic block chunks from the class's counter as in the FAST kernel
     const long long n_teams = (long long)gridDim.x * TPB;
-    const long long chunk = (ci.n_items + n_teams - 1) / n_teams;
-    const long long first = ((long long)blockIdx.x * TPB + tc.tib) * chunk;
+    const bool dyn = HAFB_DYN && ci.ctr != nullptr;
+    long long ch = (ci.n_items + n_teams - 1) / n_teams;
+    if (dyn) {
+        ch = ci.n_items / (n_teams * HAFB_DYN_PER);
+        ch = ch < 1 ? 1 : (ch > HAFB_DYN_CHUNK ? HAFB_DYN_CHUNK : ch);
+    }
+    const long long chunk = ch;
+    long long first = ((long long)blockIdx.x * TPB + tc.tib) * chunk;
     ItemCursor cur;
+    __shared__ long long dyn_base;
 
+    for (;;) {
+    if (dyn) {
+        __syncthreads();
+        if (threadIdx.x == 0) dyn_base = (long long)atomicAdd(ci.ctr, (unsigned long long)(TPB * chunk));
+        __syncthreads();
+        const long long b0 = dyn_base;
+        if (b0 >= ci.n_items) break;
+        first = b0 + (long long)tc.tib * chunk;
+    }
     for (long long it = 0; it < chunk; ++it) {
         const long long item = first + it;
         const bool valid = item < ci.n_items;
@@ -408,6 +425,8 @@ __global__ void __launch_bounds__(kModpThreads) modp_term_kernel(
         }
         if (valid && lane == 0) my_sum += ((D - MH) & 1) ? (eD ? p - eD : 0u) : eD;
         tc.sync();
+    }
+    if (!dyn) break;
     }
     if (lane == 0 && my_sum) atomicAdd(total, my_sum);
 }

@@ -61,6 +61,18 @@ __device__ __forceinline__ uint32_t unrank_mask(unsigned long long r, int m, int
     return mask;
 }
 
+// Dynamic work distribution of the class kernels (ClassItems::ctr): blocks take chunks
+// of at most HAFB_DYN_CHUNK items per team, at least HAFB_DYN_PER chunks per team.
+#ifndef HAFB_DYN
+#define HAFB_DYN 1
+#endif
+#ifndef HAFB_DYN_CHUNK
+#define HAFB_DYN_CHUNK 16
+#endif
+#ifndef HAFB_DYN_PER
+#define HAFB_DYN_PER 8
+#endif
+
 struct ItemRef {
     uint32_t mask;
     long long problem;

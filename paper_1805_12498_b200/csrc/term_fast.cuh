@@ -110,12 +110,6 @@ constexpr int kInvSlots = (kDMax + 2) & ~1;
 #ifndef HAFB_NS_HI
 #define HAFB_NS_HI 32
 #endif
-#ifndef HAFB_DYN_CHUNK
-#define HAFB_DYN_CHUNK 16
-#endif
-#ifndef HAFB_DYN_PER
-#define HAFB_DYN_PER 8
-#endif
 constexpr bool ns_variant(int S) { return HAFB_NS && S >= HAFB_NS_LO && S <= HAFB_NS_HI; }
 
 // packed upper-Hessenberg storage, column-major: column c holds rows 0..min(c+1, S-1)
@@ -1106,9 +1100,6 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
     // counter (ch items per team, walked contiguously), so the kernel's tail is one
     // chunk rather than the spread of whole-kernel team times (measured ~5 ms per big
     // class launch: 10 % of a 1/8 shard, 2-3 % of the full step).
-#ifndef HAFB_DYN
-#define HAFB_DYN 1
-#endif
     const bool dyn = HAFB_DYN && ci.ctr != nullptr;
     long long ch = (ci.n_items + n_teams - 1) / n_teams;  // static: the whole run
     if (dyn) {

@@ -532,7 +532,17 @@ __global__ void __launch_bounds__(256) terms_smem_class_kernel(
     WarpWs w = BACKEND == 0 ? carve_spec(smem + (size_t)wib * smem_warp_elems_spec(S, n_half), S, n_half)
                             : carve(smem + (size_t)wib * smem_warp_elems(S, n_half), S, n_half);
     const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
-    for (long long it = (long long)blockIdx.x * (blockDim.x >> 5) + wib; it < ci.n_items; it += nwarps) {
+    // items one at a time: from the class's counter when set (per-subset QR times vary by
+    // the sweep count, so a static interleave leaves warps idle at the end), else strided
+    const bool dyn = HAFB_DYN && ci.ctr != nullptr;
+    long long it = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
+    for (;;) {
+        if (dyn) {
+            unsigned long long g = 0;
+            if (lane == 0) g = atomicAdd(ci.ctr, 1ull);
+            it = (long long)__shfl_sync(0xffffffffu, g, 0);
+        }
+        if (it >= ci.n_items) break;
         const ItemRef ir = resolve_item(ci, it);
         cd t = mk(0.0, 0.0);
         int st = 0;
@@ -544,6 +554,7 @@ __global__ void __launch_bounds__(256) terms_smem_class_kernel(
             if (st) status[ir.out] = (int8_t)st;  // the buffer is zeroed by the host
         }
         __syncwarp();
+        if (!dyn) it += nwarps;
     }
 }
 }  // namespace hafb

@@ -523,9 +523,12 @@ int enqueue_mask_range(const cd* at, const cd* dg, int n_half, uint64_t lo, uint
     }
     uint64_t width = (hi - lo + n_chunks - 1) / n_chunks;
     int thr = 128;
-    range_kahan_kernel<<<(n_chunks + 3) / 4, thr, 0, st>>>(terms, status, lo, hi, width,
-                                                                     n_chunks, 1, count, partials,
-                                                                     fails);
+    if (arith == HAFB_ARITH_FAST)
+        range_kahan_kernel<true><<<(n_chunks + 3) / 4, thr, 0, st>>>(terms, status, lo, hi, width,
+                                                                     n_chunks, 1, count, partials, fails);
+    else
+        range_kahan_kernel<false><<<(n_chunks + 3) / 4, thr, 0, st>>>(terms, status, lo, hi, width,
+                                                                      n_chunks, 1, count, partials, fails);
     ++g_launches;
     CK(cudaGetLastError());
     return HAFB_OK;
@@ -572,8 +575,12 @@ int enqueue_range_list(const cd* at, const cd* dg, int n_half, int n_ranges, con
     }
     if (terms_done) CK(cudaEventRecord(terms_done, st));
     int thr = 128;
-    list_kahan_kernel<<<(count + 3) / 4, thr, 0, st>>>(terms, status, d_ranges, count, width,
-                                                               total, partials, fails);
+    if (arith == HAFB_ARITH_FAST)
+        list_kahan_kernel<true><<<(count + 3) / 4, thr, 0, st>>>(terms, status, d_ranges, count, width,
+                                                                 total, partials, fails);
+    else
+        list_kahan_kernel<false><<<(count + 3) / 4, thr, 0, st>>>(terms, status, d_ranges, count, width,
+                                                                  total, partials, fails);
     ++g_launches;
     CK(cudaGetLastError());
     return HAFB_OK;
@@ -994,8 +1001,12 @@ int batch_run(Call& c, const cd* d_at, const cd* d_dg, int batch, int n_half, in
     {
         int thr = 128;
         int blocks = (int)(((long long)n_ranges * batch + 3) / 4);  // one warp per range
-        range_kahan_kernel<<<blocks, thr, 0, c.st>>>(d_t, d_s, 1, total, width, n_ranges, batch,
-                                                     per, d_part, d_fail);
+        if (arith == HAFB_ARITH_FAST)
+            range_kahan_kernel<true><<<blocks, thr, 0, c.st>>>(d_t, d_s, 1, total, width, n_ranges, batch,
+                                                               per, d_part, d_fail);
+        else
+            range_kahan_kernel<false><<<blocks, thr, 0, c.st>>>(d_t, d_s, 1, total, width, n_ranges, batch,
+                                                                per, d_part, d_fail);
         ++g_launches;
         CK(cudaGetLastError());
     }

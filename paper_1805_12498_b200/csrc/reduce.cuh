@@ -75,10 +75,50 @@ __device__ __forceinline__ void warp_kahan_run(const cd* __restrict__ terms,
     }
 }
 
+// FAST arithmetic: the same range sum with the chain split over the warp's lanes (lane l
+// Kahan-sums terms l, l+32, ... with coalesced loads; the 32 compensated partials are
+// combined by a fixed butterfly), so a range costs count/32 chain steps instead of
+// count.  Deterministic for any rank count (a function of the range alone).  `fail`
+// keeps the reference's semantics: the status of the last failing term in mask order.
+__device__ __forceinline__ void warp_par_run(const cd* __restrict__ terms,
+                                             const int8_t* __restrict__ status, uint64_t q0,
+                                             uint64_t count, Kahan& k) {
+    const int lane = threadIdx.x & 31;
+    Kahan mine;
+    long long last = -1;
+    int last_st = 0;
+    for (uint64_t i = lane; i < count; i += 32) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(terms + q0 + i));
+        const int st = __ldg(reinterpret_cast<const signed char*>(status) + q0 + i);
+        mine.add(mk(v.x, v.y), 0);
+        if (st != 0) {
+            last = (long long)i;
+            last_st = st;
+        }
+    }
+    double re = mine.sre - mine.cre, im = mine.sim - mine.cim;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        re += __shfl_xor_sync(0xffffffffu, re, off);
+        im += __shfl_xor_sync(0xffffffffu, im, off);
+        const long long ol = __shfl_xor_sync(0xffffffffu, last, off);
+        const int os = __shfl_xor_sync(0xffffffffu, last_st, off);
+        if (ol > last) {
+            last = ol;
+            last_st = os;
+        }
+    }
+    k.sre = re;
+    k.sim = im;
+    k.cre = k.cim = 0.0;
+    k.fail = last_st;
+}
+
 // Batched over `batch` problems whose terms are `per` apart.
 // Kahan per chunk over masks [lo + r*width, min(lo + (r+1)*width, hi)); terms are
 // indexed by mask - lo.  Mask 0 is skipped.  fails[r] keeps the reference's
 // "last nonzero status in the range" semantics.
+template <bool PAR = false>
 __global__ void __launch_bounds__(128) range_kahan_kernel(const cd* __restrict__ terms,
                                                           const int8_t* __restrict__ status,
                                                           uint64_t lo, uint64_t hi, uint64_t width,
@@ -96,7 +136,10 @@ __global__ void __launch_bounds__(128) range_kahan_kernel(const cd* __restrict__
     if (b > hi) b = hi;
     if (a == 0 && b > 0) a = 1;  // mask 0 is skipped
     Kahan k;
-    if (b > a) warp_kahan_run(terms, status, a - lo, b - a, k, stage[threadIdx.x >> 5]);
+    if (b > a) {
+        if constexpr (PAR) warp_par_run(terms, status, a - lo, b - a, k);
+        else warp_kahan_run(terms, status, a - lo, b - a, k, stage[threadIdx.x >> 5]);
+    }
     if ((threadIdx.x & 31) == 0) {
         partials[g] = mk(k.sre, k.sim);
         fails[g] = k.fail;
@@ -127,6 +170,7 @@ __global__ void __launch_bounds__(128) worker_kahan_kernel(const cd* __restrict_
 
 // Range-list mode: partial p sums terms [p*width, (p+1)*width) of the buffer, whose
 // masks are 1 + ranges[p]*width + offset; masks >= total are padding.
+template <bool PAR = false>
 __global__ void __launch_bounds__(128) list_kahan_kernel(const cd* __restrict__ terms,
                                                          const int8_t* __restrict__ status,
                                                          const int32_t* __restrict__ ranges, int count,
@@ -139,7 +183,8 @@ __global__ void __launch_bounds__(128) list_kahan_kernel(const cd* __restrict__ 
     uint64_t first = 1 + (uint64_t)ranges[p] * width;
     const uint64_t n = first >= total ? 0 : (total - first < width ? total - first : width);
     Kahan k;
-    warp_kahan_run(terms, status, (uint64_t)p * width, n, k, stage[threadIdx.x >> 5]);
+    if constexpr (PAR) warp_par_run(terms, status, (uint64_t)p * width, n, k);
+    else warp_kahan_run(terms, status, (uint64_t)p * width, n, k, stage[threadIdx.x >> 5]);
     if ((threadIdx.x & 31) == 0) {
         partials[p] = mk(k.sre, k.sim);
         fails[p] = k.fail;

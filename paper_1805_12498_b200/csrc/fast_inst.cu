@@ -44,8 +44,14 @@ constexpr bool fast_spectral_ok(int S, bool loops) {
 #ifndef HAFB_REG_THREADS
 #define HAFB_REG_THREADS 384
 #endif
-constexpr int threads_for(int S) {
-    return ns_variant(S) ? (S > 32 ? HAFB_NS_WIDE_THREADS : S <= 16 ? kFastThreads : S <= 22 ? HAFB_NS_SMALL_THREADS : HAFB_REG_THREADS)
+// Split rows (term_fast.cuh, ns_split_k): the no-loop static-column classes S = 24..28
+// keep part of each row in shared memory and run 16 teams per SM.
+#ifndef HAFB_SPLIT_HI
+#define HAFB_SPLIT_HI 28
+#endif
+constexpr int threads_for(int S, bool loops) {
+    return ns_variant(S) ? (S > 32 ? HAFB_NS_WIDE_THREADS : S <= 16 ? kFastThreads : S <= 22 ? HAFB_NS_SMALL_THREADS
+                            : (!loops && S >= HAFB_NS_SPLIT_LO && S <= HAFB_SPLIT_HI) ? 512 : HAFB_REG_THREADS)
            : !smem_hess(S) && S >= 26 ? (S > 32 ? 256 : HAFB_REG_THREADS)
            : S > 32 ? 64  // 64-lane teams: one team per block (register-limited: 5 teams/SM, not 4)
            : smem_hess(S) ? 32  // one team per block: the register file packs one more team
@@ -63,7 +69,7 @@ static cudaError_t launch_one(const cd* at, const cd* dg, int n_half, const Clas
     constexpr bool NSX = nsx_variant(S) && !L;
     constexpr bool SH = smem_hess(S) && !NSX;
     constexpr int W = FastTeam<S, L, SH>::W;
-    constexpr int NT = NSX ? HAFB_NSX_THREADS : threads_for(S);
+    constexpr int NT = NSX ? HAFB_NSX_THREADS : threads_for(S, L);
     constexpr int TPB = NT / W;
     const size_t base_smem = (size_t)TPB * FastLayout<S, SH, L>::TOTAL * sizeof(cd) + kInvSlots * sizeof(double);
     // the one-block-per-SM register classes stage Atilde in shared memory when it fits

@@ -122,8 +122,11 @@ struct FastLayout {
     static constexpr int SP = S + 12;                  // padded pivot-row / multiplier length
     static constexpr int PR = HS + (SH ? S * S : hs_elems(S));  // [2][SP] pivot rows (register variant)
     // [2][SP] multipliers (the window variant for S >= 26 shuffles the pivot row: no PR)
-    static constexpr int MU = PR + ((SH || (HAFB_SHFL_PIVOT && S >= 26 && !HAFB_NS)) ? 0 : 2 * SP);
-    static constexpr int CF = MU + 2 * SP;            // [2][S] charpoly coefs
+    // S = 28 (static-column kernel, one pivot-row and one multiplier buffer): single
+    // buffers, so 16 teams and the staged Atilde of n <= 56 fit one SM's shared memory
+    static constexpr bool TRIM = !SH && S == 28 && HAFB_NS;
+    static constexpr int MU = PR + ((SH || (HAFB_SHFL_PIVOT && S >= 26 && !HAFB_NS)) ? 0 : TRIM ? SP : 2 * SP);
+    static constexpr int CF = MU + (TRIM ? SP : 2 * SP);  // [2][S] charpoly coefs
     static constexpr int RED = CF + 2 * S;            // [2][2][2] argmax exchange (W = 64)
     static constexpr int A = RED + 8;                 // [S+1] charpoly coefficients
     static constexpr int U = A + S + 1;               // [2][S] loop-chain vector (LOOPS)
@@ -603,9 +606,31 @@ __device__ __forceinline__ void ns_read(const cd (&w)[S], int b, cd& v) {
 }
 
 
-template <int S, int W>
+// Split rows (K > 2, one-warp teams): logical columns 2..K-1 of every lane row live in
+// shared memory (slot [c][lane] at the top of the packed-Hessenberg region) instead of
+// registers.  Those columns retire first -- column c leaves the sweep after step c-2 --
+// so they carry a small share of the sweep's column-steps (16 % at S = 28, K = 12),
+// while the 4(K-2) registers saved per lane lift the class from 12 to 16 warps per SM
+// (the register file is the occupancy limit).
+template <int S, int K>
+struct NsSplit {
+    static_assert(K == 2 || (K > 2 && K <= S), "split bound");
+    // Hq[c * 32 + lane] for 2 <= c < K
+    static constexpr int BASE = hs_elems(S) - (K - 2) * 32 - 2 * 32;
+    // the packed column retired at step J (slots J(J+3)/2 .. +J+1) stays below the
+    // split columns still live at that step (J+2 .. K-1)
+    static constexpr bool disjoint() {
+        for (int J = 0; J + 2 < K; ++J)
+            if ((J * (J + 3)) / 2 + J + 1 >= BASE + (J + 2) * 32) return false;
+        return BASE >= 0;
+    }
+    static_assert(K == 2 || disjoint(), "split overlaps the packed store");
+};
+
+template <int S, int W, int K = 2>
 __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const TeamCtx<W>& tc, cd* ws) {
     static_assert(W == 16 || W == 32 || W == 64, "NS variant: half-warp, one- or two-warp teams");
+    static_assert(K == 2 || W == 32, "split rows: one-warp teams");
     // W = 16: two teams per warp (team mask / lane base); their uniform branches may diverge
     const unsigned tm = W < 32 ? tc.wmask : 0xffffffffu;
     const int tb = W < 32 ? ((int)(threadIdx.x & 31) & ~(W - 1)) : 0;
@@ -614,6 +639,16 @@ __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const Team
     cd* pr = ws + L::PR;  // pivot row, by logical column
     cd* mus = ws + L::MU;  // multiplier of each logical row
     const int lane = tc.lane;
+    cd* Hq = Hs + NsSplit<S, K>::BASE;  // split columns: Hq[c * 32 + lane], 2 <= c < K
+    // hn = logical column b of the lane's row (b >= 2, team-uniform)
+    auto col_read = [&](int b, cd& v) {
+        if constexpr (K > 2) {
+            if (b < K) v = Hq[b * 32 + lane];
+            else ns_read<S, K, S>(w, b, v);
+        } else {
+            ns_read<S, 2, S>(w, b, v);
+        }
+    };
     cd hj = w[0], hn = w[1];
     HT_DECL
 #pragma unroll 1
@@ -662,7 +697,7 @@ __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const Team
         if ((mx & ~63u) == 0u) {  // nothing to eliminate below the subdiagonal: no update
             if (myrow <= J + 1) Hs[CS + myrow] = hj;
             hj = hn;
-            ns_read<S, 2, S>(w, J + 2, hn);
+            col_read(J + 2, hn);
             continue;
         }
 #if NS_SPECINV
@@ -697,7 +732,20 @@ __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const Team
 #endif
         if (myrow <= J + 1) Hs[CS + myrow] = hj;
         // column swap J+1 <-> brow: column J+1 is hn, column brow >= J+2 sits at w[brow]
-        if (brow != J + 1) ns_xchg<S, 2, S>(w, brow, hn);  // (a switch jump table: 6x slower)
+        if (brow != J + 1) {  // (a switch jump table: 6x slower)
+            if constexpr (K > 2) {
+                if (brow < K) {
+                    cd* q = Hq + brow * 32 + lane;
+                    const cd t = *q;
+                    *q = hn;
+                    hn = t;
+                } else {
+                    ns_xchg<S, K, S>(w, brow, hn);
+                }
+            } else {
+                ns_xchg<S, 2, S>(w, brow, hn);
+            }
+        }
         // publish the pivot row (logical row J+1): its lane stores columns J+1 .. S-1, one
         // exit test per pair (measured alternatives: stores predicated over every column
         // +10 %; a jump into a straight run of stores +5 %; register shuffles of the pivot
@@ -709,8 +757,16 @@ __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const Team
             const bool pl = lane == wl;
             static_for<0, S - 2, 2>([&](auto ii) {
                 constexpr int c = S - 1 - decltype(ii)::value;
-                if (pl) pr[c] = w[c];
-                if (c - 1 >= J + 2 && pl) pr[c - 1] = w[c - 1];
+                if constexpr (c >= K) {
+                    if (pl) pr[c] = w[c];
+                } else {
+                    if (pl) pr[c] = Hq[c * 32 + lane];
+                }
+                if constexpr (c - 1 >= K) {
+                    if (c - 1 >= J + 2 && pl) pr[c - 1] = w[c - 1];
+                } else {
+                    if (c - 1 >= J + 2 && pl) pr[c - 1] = Hq[(c - 1) * 32 + lane];
+                }
                 if (c - 1 <= J + 2) return false;
                 return true;
             });
@@ -737,17 +793,23 @@ __device__ __forceinline__ void ns_hessenberg(cd (&w)[S], int& myrow, const Team
         static_for<0, S - 2>([&](auto ii) {
             constexpr int c = S - 1 - decltype(ii)::value;
             const cd pn = pr[c - 1], mn = mus[c - 1];  // next column's broadcasts (c-1 >= 1)
-            w[c] = f_cms(w[c], mu, pa);
-            if constexpr (c & 1) acc1 = f_cma(acc1, ma, w[c]);
-            else acc0 = f_cma(acc0, ma, w[c]);
+            cd x;
+            if constexpr (c >= K) {
+                w[c] = f_cms(w[c], mu, pa);
+                x = w[c];
+            } else {
+                x = f_cms(Hq[c * 32 + lane], mu, pa);
+            }
+            if constexpr (c & 1) acc1 = f_cma(acc1, ma, x);
+            else acc0 = f_cma(acc0, ma, x);
             pa = pn;
             ma = mn;
             if (c == J + 2) {
-                const cd nh = w[c];
                 hj = f_add(f_cms(hn, mu, pa), f_add(acc0, acc1));  // pa = pr[J+1]
-                hn = nh;
+                hn = x;  // (a split column's slot is dead from here on)
                 return false;
             }
+            if constexpr (c < K) Hq[c * 32 + lane] = x;
             return true;
         });
         HT_MARK(11);
@@ -1044,6 +1106,21 @@ __device__ __forceinline__ void nsx_hessenberg(cd (&w)[S], cd (&ex)[S - 32], int
 #include "qr_fast.cuh"
 namespace hafb {
 
+// split-row bound K of the static-column classes (ns_hessenberg): one-warp teams in
+// blocks of >= 512 threads (16 teams, <= 128 registers) keep HAFB_NS_KEEP columns
+// (K..S-1) of the lane's row in registers, columns 2..K-1 in shared memory
+#ifndef HAFB_NS_KEEP
+#define HAFB_NS_KEEP 16
+#endif
+#ifndef HAFB_NS_SPLIT_LO
+#define HAFB_NS_SPLIT_LO 24
+#endif
+constexpr int ns_split_k(int S, bool loops, bool sh, int nt) {
+    return (ns_variant(S) && !loops && !sh && S >= HAFB_NS_SPLIT_LO && S <= 32 && nt >= 512 && S - HAFB_NS_KEEP > 2)
+               ? S - HAFB_NS_KEEP
+               : 2;
+}
+
 template <int S, bool LOOPS, bool SH>
 struct FastTeam {
     static constexpr bool NSX = nsx_variant(S) && !LOOPS && !SH;
@@ -1071,6 +1148,7 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
     constexpr bool PSYNC = NT > kFastThreads && (NSX || (HAFB_PSYNC && (!ns_variant(S) || HAFB_PSYNC_NS)));
     constexpr int W = FastTeam<S, LOOPS, SH>::W;
     constexpr int TPB = NT / W;
+    constexpr int NSK = ns_split_k(S, LOOPS, SH, NT);
     constexpr int M = S / 2;
     constexpr int R = (kDMax + W - 1) / W;  // coefficient chunks per lane
     using L = FastLayout<S, SH, LOOPS>;
@@ -1260,16 +1338,21 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
             HT_MARK(0);
             nsx_hessenberg<S>(hr, ex, myrow, elab, tc, ws);
         } else {
+            constexpr int K = NSK;
+            cd* Hq = ws + L::HS + NsSplit<S, K>::BASE;
+            if constexpr (K > 2) tc.sync();  // the previous subset's readers of the region
             gather([&](const cd* src, int ld) {
                 static_for<0, S>([&](auto c) {
                     const int vc = 2 * vbit[c() >> 1] + (c() & 1);
-                    hr[c()] = lane < S ? src[vr * ld + vc] : mk(0.0, 0.0);
+                    const cd v = lane < S ? src[vr * ld + vc] : mk(0.0, 0.0);
+                    if constexpr (c() >= 2 && c() < K) Hq[c() * 32 + lane] = v;
+                    else hr[c()] = v;
                     return true;
                 });
             });
             HT_MARK(0);
             // ---------------------------------------------- Hessenberg (_numba.py:36-67)
-            if constexpr (ns_variant(S)) ns_hessenberg<S, W>(hr, myrow, tc, ws);
+            if constexpr (ns_variant(S)) ns_hessenberg<S, W, K>(hr, myrow, tc, ws);
             else fast_hessenberg<S, W>(hr, myrow, tc, ws);
         }
         HT_MARK(1);

@@ -433,14 +433,18 @@ __global__ void __launch_bounds__(kMirrorThreads, mirror_minb<S>()) mirror_term_
         tc.sync();
         HT_MARK(3);
         // ------------------------------------------------ _exp_top (_numba.py:276-294), Horner
+        // Only E[D] is returned, and F[d] reads E[0..d-1]: at step jj the coefficients
+        // d > D - jj + 1 never reach E[D], so they are not computed (the ones that are
+        // computed are the same operation sequences: bit-identical, half the chain).
         for (int jj = D; jj > 0; --jj) {
             const double inv = INVJ[jj];  // = r_div(1.0, jj)
+            const int dmax = D - jj + 1;
             cd f[(kDMax + W) / W];
 #pragma unroll
             for (int r = 0; r < (kDMax + W) / W; ++r) {
                 const int d = lane + W * r;
                 f[r] = mk(0.0, 0.0);
-                if (d <= D) {
+                if (d <= dmax) {
                     cd acc = mk(0.0, 0.0);
                     for (int tt = 1; tt <= d; ++tt) acc = m_add(acc, m_mul(E[d - tt], SSr[tt]));
                     f[r] = m_rmul(inv, acc);
@@ -451,7 +455,7 @@ __global__ void __launch_bounds__(kMirrorThreads, mirror_minb<S>()) mirror_term_
 #pragma unroll
             for (int r = 0; r < (kDMax + W) / W; ++r) {
                 const int d = lane + W * r;
-                if (d <= D) E[d] = f[r];
+                if (d <= dmax) E[d] = f[r];
             }
             tc.sync();
         }

@@ -446,12 +446,15 @@ __device__ inline void subset_term_smem(const cd* __restrict__ atilde, const cd*
     const int D = K;
     for (int d = lane; d <= D; d += 32) w.E[d] = (d == 0) ? mk(1.0, 0.0) : mk(0.0, 0.0);
     __syncwarp();
+    // (only E[D] is returned: at step j the coefficients d > D - j + 1 never reach it and
+    // are skipped; the computed ones keep their operation sequences)
     for (int j = D; j > 0; --j) {
         double inv = r_div(1.0, (double)j);
+        const int dmax = D - j + 1;
         cd f[2] = {mk(0.0, 0.0), mk(0.0, 0.0)};
         for (int q = 0; q < 2; ++q) {
             const int d = lane + 32 * q;
-            if (d <= D) {
+            if (d <= dmax) {
                 cd acc = mk(0.0, 0.0);
                 for (int tt = 1; tt <= d; ++tt) acc = m_add(acc, m_mul(w.E[d - tt], w.s[tt]));
                 f[q] = m_rmul(inv, acc);
@@ -460,7 +463,7 @@ __device__ inline void subset_term_smem(const cd* __restrict__ atilde, const cd*
         }
         __syncwarp();
         for (int q = 0; q < 2; ++q)
-            if (lane + 32 * q <= D) w.E[lane + 32 * q] = f[q];
+            if (lane + 32 * q <= dmax) w.E[lane + 32 * q] = f[q];
         __syncwarp();
     }
     cd coeff = w.E[D];

@@ -62,14 +62,26 @@ constexpr int threads_for(int S, bool loops) {
 #define HAFB_NSX_THREADS 256
 #endif
 
-template <int S, bool L, bool SPEC = false>
+// NSX classes with split rows (term_fast.cuh, nsx_split_k): blocks of 11-12 teams at <= 168
+// registers, tried from the largest down until the workspaces and the staged Atilde fit one
+// SM's shared memory: S = 34 runs 12 teams up to n = 52 (167.7 -> 146.0 ms at n = 52) and 11
+// up to n = 60 (-4 % at n = 56); S = 36 runs 11 teams up to n = 52 (-6 %; 10 teams measured
+// 2 % slower than the unsplit kernel).  The unsplit 256-thread kernel (8 teams) is the last
+// level and the FAST spectral configuration.
+constexpr int nsx_threads(int S, bool spec, int level) {
+    if (spec || nsx_split_k(S, 384) <= 2) return HAFB_NSX_THREADS;
+    if (S == 34) return level == 0 ? 384 : level == 1 ? 352 : HAFB_NSX_THREADS;
+    return level == 0 ? 352 : HAFB_NSX_THREADS;
+}
+
+template <int S, bool L, bool SPEC = false, int LEVEL = 0>
 static cudaError_t launch_one(const cd* at, const cd* dg, int n_half, const ClassItems& ci,
                               cd* terms, int8_t* status, cudaStream_t st, int sms, int cap = 0) {
     // S = 34, 36 without loops: one-warp teams with the extra rows held column-wise
     constexpr bool NSX = nsx_variant(S) && !L;
     constexpr bool SH = smem_hess(S) && !NSX;
     constexpr int W = FastTeam<S, L, SH>::W;
-    constexpr int NT = NSX ? HAFB_NSX_THREADS : threads_for(S, L);
+    constexpr int NT = NSX ? nsx_threads(S, SPEC, LEVEL) : threads_for(S, L);
     constexpr int TPB = NT / W;
     const size_t base_smem = (size_t)TPB * FastLayout<S, SH, L>::TOTAL * sizeof(cd) + kInvSlots * sizeof(double);
     // the one-block-per-SM register classes stage Atilde in shared memory when it fits
@@ -77,6 +89,9 @@ static cudaError_t launch_one(const cd* at, const cd* dg, int n_half, const Clas
     const size_t a_bytes = (size_t)n * (n + 1) * sizeof(cd);
     const int optin = device_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin);
     const int stage = (NT > kFastThreads && !SH && base_smem + a_bytes <= (size_t)optin) ? 1 : 0;
+    if constexpr (NSX && NT != HAFB_NSX_THREADS) {
+        if (!stage) return launch_one<S, L, SPEC, LEVEL + 1>(at, dg, n_half, ci, terms, status, st, sms, cap);
+    }
     const size_t smem = base_smem + (stage ? a_bytes : 0);
     auto kern = fast_term_kernel<S, L, SH, NT, SPEC>;
     // smem depends on n (the staged Atilde): the attribute is the size-independent

@@ -125,18 +125,21 @@ struct FastLayout {
     // S = 28 (static-column kernel, one pivot-row and one multiplier buffer): single
     // buffers, so 16 teams and the staged Atilde of n <= 56 fit one SM's shared memory
     static constexpr bool TRIM = !SH && S == 28 && HAFB_NS;
-    static constexpr int MU = PR + ((SH || (HAFB_SHFL_PIVOT && S >= 26 && !HAFB_NS)) ? 0 : TRIM ? SP : 2 * SP);
+    // S = 34, 36 (NSX with split rows, 10-12 teams): one pivot-row buffer; the second multiplier
+    // buffer stays (the tensor-core charpoly stages T in this scratch and needs the room)
+    static constexpr bool TRIM_PR = TRIM || (!SH && !LOOPS && (S == 34 || S == 36) && HAFB_NS);
+    static constexpr int MU = PR + ((SH || (HAFB_SHFL_PIVOT && S >= 26 && !HAFB_NS)) ? 0 : TRIM_PR ? SP : 2 * SP);
     static constexpr int CF = MU + (TRIM ? SP : 2 * SP);  // [2][S] charpoly coefs
     static constexpr int RED = CF + 2 * S;            // [2][2][2] argmax exchange (W = 64)
     static constexpr int A = RED + 8;                 // [S+1] charpoly coefficients
     static constexpr int U = A + S + 1;               // [2][S] loop-chain vector (LOOPS)
     static constexpr int PX = U + (LOOPS ? 2 * S : 0);  // [S] cross-warp exchange (W = 64)
-    static constexpr int T = PX + (S > 32 ? S : 4);   // [kDMax+2] traces / exp broadcast
+    static constexpr int T = PX + ((S > 32 && (SH || LOOPS)) ? S : 4);  // [kDMax+2] traces / exp broadcast (PX: two-warp teams only)
     static constexpr int G = T + kDMax + 2;           // [kDMax+2] g_j = j s_j
     static constexpr int FLAG = G + kDMax + 2;        // [1]
     static constexpr int SIGN = (S + 3) / 4 + 1;      // cd slots holding S ints
     static constexpr int SIG = FLAG + 2;              // [2][S] int: logical row -> lane (SH)
-    static constexpr int CRN = SIG + 2 * SIGN;        // NSX: the extra rows' columns >= 32 ([E][E])
+    static constexpr int CRN = SIG + (SH ? 2 * SIGN : 0);  // NSX: the extra rows' columns >= 32 ([E][E])
     static constexpr int TOTAL = CRN + (S > 32 ? (S - 32) * (S - 32) : 0);
 };
 
@@ -881,7 +884,7 @@ __device__ __forceinline__ void nsx_allreduce(cd (&v)[E], int lane) {
     }
 }
 
-template <int S>
+template <int S, int K = 2>
 __device__ __forceinline__ void nsx_hessenberg(cd (&w)[S], cd (&ex)[S - 32], int& myrow,
                                                int (&elab)[S - 32], const TeamCtx<32>& tc, cd* ws) {
     constexpr int E = S - 32;
@@ -891,6 +894,17 @@ __device__ __forceinline__ void nsx_hessenberg(cd (&w)[S], cd (&ex)[S - 32], int
     cd* mus = ws + L::MU;
     cd* CR = ws + L::CRN;  // CR[e * E + q] = h(32 + e, 32 + q)
     const int lane = tc.lane;
+    // split rows (K > 2, as in ns_hessenberg): logical columns 2..K-1 of the lane rows in
+    // shared memory, so the class fits 168 registers and 12 teams per SM instead of 8
+    cd* Hq = Hs + NsSplit<S, K>::BASE;
+    auto col_read = [&](int b, cd& v) {
+        if constexpr (K > 2) {
+            if (b < K) v = Hq[b * 32 + lane];
+            else ns_read<S, K, S>(w, b, v);
+        } else {
+            ns_read<S, 2, S>(w, b, v);
+        }
+    };
     cd hj = w[0], hn = w[1];
     __syncwarp();
 #pragma unroll 1
@@ -925,7 +939,7 @@ __device__ __forceinline__ void nsx_hessenberg(cd (&w)[S], cd (&ex)[S - 32], int
                     if (elab[e] <= J + 1) Hs[CS + elab[e]] = xv[e];
             }
             hj = hn;
-            ns_read<S, 2, S>(w, J + 2, hn);
+            col_read(J + 2, hn);
             continue;
         }
         int brow;
@@ -969,7 +983,18 @@ __device__ __forceinline__ void nsx_hessenberg(cd (&w)[S], cd (&ex)[S - 32], int
         // column swap J+1 <-> brow: lane rows by the register tree; extra rows by a
         // shuffle pair (both columns < 32) or a corner exchange
         if (brow != J + 1) {
-            ns_xchg<S, 2, S>(w, brow, hn);
+            if constexpr (K > 2) {
+                if (brow < K) {
+                    cd* q = Hq + brow * 32 + lane;
+                    const cd t = *q;
+                    *q = hn;
+                    hn = t;
+                } else {
+                    ns_xchg<S, K, S>(w, brow, hn);
+                }
+            } else {
+                ns_xchg<S, 2, S>(w, brow, hn);
+            }
             const int a = J + 1, b = brow;  // a < b
             if (b < 32) {
                 const int src = lane == a ? b : a;
@@ -1004,8 +1029,16 @@ __device__ __forceinline__ void nsx_hessenberg(cd (&w)[S], cd (&ex)[S - 32], int
             const bool pl = lane == pw;
             static_for<0, S - 2, 2>([&](auto ii) {
                 constexpr int c = S - 1 - decltype(ii)::value;
-                if (pl) pr[c] = w[c];
-                if (c - 1 >= J + 2 && pl) pr[c - 1] = w[c - 1];
+                if constexpr (c >= K) {
+                    if (pl) pr[c] = w[c];
+                } else {
+                    if (pl) pr[c] = Hq[c * 32 + lane];
+                }
+                if constexpr (c - 1 >= K) {
+                    if (c - 1 >= J + 2 && pl) pr[c - 1] = w[c - 1];
+                } else {
+                    if (c - 1 >= J + 2 && pl) pr[c - 1] = Hq[(c - 1) * 32 + lane];
+                }
                 if (c - 1 <= J + 2) return false;
                 return true;
             });
@@ -1029,17 +1062,23 @@ __device__ __forceinline__ void nsx_hessenberg(cd (&w)[S], cd (&ex)[S - 32], int
         static_for<0, S - 2>([&](auto ii) {
             constexpr int c = S - 1 - decltype(ii)::value;
             const cd pn = pr[c - 1], mn = mus[c - 1];
-            w[c] = f_cms(w[c], mu, pa);
-            if constexpr (c & 1) acc1 = f_cma(acc1, ma, w[c]);
-            else acc0 = f_cma(acc0, ma, w[c]);
+            cd x;
+            if constexpr (c >= K) {
+                w[c] = f_cms(w[c], mu, pa);
+                x = w[c];
+            } else {
+                x = f_cms(Hq[c * 32 + lane], mu, pa);
+            }
+            if constexpr (c & 1) acc1 = f_cma(acc1, ma, x);
+            else acc0 = f_cma(acc0, ma, x);
             pa = pn;
             ma = mn;
             if (c == J + 2) {
-                const cd nh = w[c];
                 hj = f_add(f_cms(hn, mu, pa), f_add(acc0, acc1));
-                hn = nh;
+                hn = x;  // (a split column's slot is dead from here on)
                 return false;
             }
+            if constexpr (c < K) Hq[c * 32 + lane] = x;
             return true;
         });
         // extra rows: rank-1 update of my live columns (c >= J+1) and the gemv partials.
@@ -1121,6 +1160,21 @@ constexpr int ns_split_k(int S, bool loops, bool sh, int nt) {
                : 2;
 }
 
+// split-row bound of the NSX classes (nsx_hessenberg) in blocks of 352..384 threads (11-12
+// teams, <= 168 registers): columns 2..K-1 of the lane rows in shared memory; 2 = no split
+#ifndef HAFB_NSX_K34
+#define HAFB_NSX_K34 10
+#endif
+#ifndef HAFB_NSX_K36
+#define HAFB_NSX_K36 20
+#endif
+#ifndef HAFB_NSX_K38
+#define HAFB_NSX_K38 2
+#endif
+constexpr int nsx_split_k(int S, int nt) {
+    return nt < 320 ? 2 : S == 34 ? HAFB_NSX_K34 : S == 36 ? HAFB_NSX_K36 : S == 38 ? HAFB_NSX_K38 : 2;
+}
+
 template <int S, bool LOOPS, bool SH>
 struct FastTeam {
     static constexpr bool NSX = nsx_variant(S) && !LOOPS && !SH;
@@ -1148,7 +1202,7 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
     constexpr bool PSYNC = NT > kFastThreads && (NSX || (HAFB_PSYNC && (!ns_variant(S) || HAFB_PSYNC_NS)));
     constexpr int W = FastTeam<S, LOOPS, SH>::W;
     constexpr int TPB = NT / W;
-    constexpr int NSK = ns_split_k(S, LOOPS, SH, NT);
+    constexpr int NSK = NSX ? nsx_split_k(S, NT) : ns_split_k(S, LOOPS, SH, NT);
     constexpr int M = S / 2;
     constexpr int R = (kDMax + W - 1) / W;  // coefficient chunks per lane
     using L = FastLayout<S, SH, LOOPS>;
@@ -1320,10 +1374,15 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
             // column lane in registers, columns 32+q (q < E) in the shared-memory corner
             const int cb1 = lane < E ? (int)__fns(ir.mask, 0, 16 + (lane >> 1) + 1) : 0;
             cd* CR = ws + L::CRN;
+            constexpr int K = NSK;
+            cd* Hq = ws + L::HS + NsSplit<S, K>::BASE;
+            if constexpr (K > 2) tc.sync();  // the previous subset's readers of the region
             gather([&](const cd* src, int ld) {
                 static_for<0, S>([&](auto c) {
                     const int vc = 2 * vbit[c() >> 1] + (c() & 1);
-                    hr[c()] = src[vr * ld + vc];
+                    const cd v = src[vr * ld + vc];
+                    if constexpr (c() >= 2 && c() < K) Hq[c() * 32 + lane] = v;
+                    else hr[c()] = v;
                     return true;
                 });
                 static_for<0, E>([&](auto ee) {
@@ -1336,7 +1395,7 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
                 });
             });
             HT_MARK(0);
-            nsx_hessenberg<S>(hr, ex, myrow, elab, tc, ws);
+            nsx_hessenberg<S, K>(hr, ex, myrow, elab, tc, ws);
         } else {
             constexpr int K = NSK;
             cd* Hq = ws + L::HS + NsSplit<S, K>::BASE;

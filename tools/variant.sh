@@ -5,7 +5,7 @@
 NAME=$1; FLAGS=$2; shift 2
 DEF=$(ls -d build/obj-* | head -1)
 [ -n "$HAFB_DEFAULT_OBJ" ] && DEF=$HAFB_DEFAULT_OBJ
-OUT=build_variants/obj-$NAME; mkdir -p $OUT
+OUT=build/variant-obj-$NAME; mkdir -p $OUT
 cp -u $DEF/*.o $OUT/
 for S in "$@"; do
   SS=$(printf %02d $S)

@@ -70,8 +70,7 @@ constexpr int threads_for(int S, bool loops) {
 // level and the FAST spectral configuration.
 constexpr int nsx_threads(int S, bool spec, int level) {
     if (spec || nsx_split_k(S, 384) <= 2) return HAFB_NSX_THREADS;
-    if (S == 34) return level == 0 ? 384 : level == 1 ? 352 : HAFB_NSX_THREADS;
-    return level == 0 ? 352 : HAFB_NSX_THREADS;
+    return level == 0 ? 384 : level == 1 ? 352 : HAFB_NSX_THREADS;
 }
 
 template <int S, bool L, bool SPEC = false, int LEVEL = 0>
@@ -88,11 +87,19 @@ static cudaError_t launch_one(const cd* at, const cd* dg, int n_half, const Clas
     const int n = 2 * n_half;
     const size_t a_bytes = (size_t)n * (n + 1) * sizeof(cd);
     const int optin = device_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin);
-    const int stage = (NT > kFastThreads && !SH && base_smem + a_bytes <= (size_t)optin) ? 1 : 0;
+    // stage 1: the full Atilde (row stride n+1); stage 2 (one problem, no loops, S >= 30): the
+    // lower triangle of the symmetric A it was built from -- half the bytes, verified by every
+    // block while it stages (term_fast.cuh)
+    const size_t tri_bytes = (size_t)n * (n + 1) / 2 * sizeof(cd);
+    const bool tri_ok = !L && !SH && S >= 30 && ci.n_items == ci.per_problem;
+    const int stage = !(NT > kFastThreads && !SH)                ? 0
+                      : base_smem + a_bytes <= (size_t)optin      ? 1
+                      : tri_ok && base_smem + tri_bytes <= (size_t)optin ? 2
+                                                                         : 0;
     if constexpr (NSX && NT != HAFB_NSX_THREADS) {
         if (!stage) return launch_one<S, L, SPEC, LEVEL + 1>(at, dg, n_half, ci, terms, status, st, sms, cap);
     }
-    const size_t smem = base_smem + (stage ? a_bytes : 0);
+    const size_t smem = base_smem + (stage == 1 ? a_bytes : stage == 2 ? tri_bytes : 0);
     auto kern = fast_term_kernel<S, L, SH, NT, SPEC>;
     // smem depends on n (the staged Atilde): the attribute is the size-independent
     // opt-in maximum, so host threads launching different n never race on it

@@ -1247,10 +1247,30 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
     const int ldA = n + 1;
     long long staged_problem = -1;
     const long long block_first = (long long)blockIdx.x * TPB * chunk;
+    // stage_a == 2 (one problem, no loops): triangular staging.  Atilde = X A with A symmetric
+    // satisfies Atilde[r][c] == Atilde[c^1][r^1]; then only A's lower triangle is kept
+    // (A[a][b] = Atilde[a^1][b] at As[a(a+1)/2 + b], a >= b): half the bytes, so more teams fit
+    // one SM.  Every block verifies the identity bit for bit while it stages; an asymmetric
+    // input (never produced by the engines, but legal at the C ABI) is gathered from global
+    // memory instead.
+    constexpr bool TRI_OK = !LOOPS && !SH && S >= 30;
+    const bool tri = TRI_OK && stage_a == 2;
     if (stage_a && (dyn || block_first < ci.n_items)) {  // (static) a block past the last item stages nothing
         staged_problem = dyn ? 0 : block_first / ci.per_problem;
         const cd* src = atilde + staged_problem * ci.at_stride;
-        for (int i = threadIdx.x; i < n * n; i += blockDim.x) As[(i / n) * ldA + (i % n)] = src[i];
+        if (tri) {
+            int bad = 0;
+            for (int i = threadIdx.x; i < n * n; i += blockDim.x) {
+                const int r = i / n, c = i % n, a = r ^ 1;
+                const cd v = src[i], u = src[(c ^ 1) * n + a];
+                bad |= (__double_as_longlong(v.re) != __double_as_longlong(u.re)) |
+                       (__double_as_longlong(v.im) != __double_as_longlong(u.im));
+                if (a >= c) As[(a * (a + 1)) / 2 + c] = v;
+            }
+            if (__syncthreads_or(bad)) staged_problem = -1;
+        } else {
+            for (int i = threadIdx.x; i < n * n; i += blockDim.x) As[(i / n) * ldA + (i % n)] = src[i];
+        }
     }
     __syncthreads();
     ItemCursor cur;
@@ -1271,7 +1291,7 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
         if (b0 >= ci.n_items) break;
         first = b0 + (long long)tc.tib * chunk;
         // a batch: re-stage Atilde when the block's chunk starts in another problem
-        if (stage_a && b0 / ci.per_problem != staged_problem) {
+        if (stage_a == 1 && b0 / ci.per_problem != staged_problem) {
             staged_problem = b0 / ci.per_problem;
             const cd* src = atilde + staged_problem * ci.at_stride;
             for (int i = threadIdx.x; i < n * n; i += blockDim.x) As[(i / n) * ldA + (i % n)] = src[i];
@@ -1289,8 +1309,21 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
         // memory (team-uniform choice; each call site is instantiated for both spaces
         // so the loads stay LDS / LDG instead of generic)
         auto gather = [&](auto&& body) {
-            if (from_smem) body(static_cast<const cd*>(As), ldA);
-            else body(at, n);
+            if (from_smem) {
+                if constexpr (TRI_OK) {
+                    if (tri) {
+                        body([&](int r, int c) -> cd {
+                            const int a = r ^ 1;
+                            const int hi = a > c ? a : c, lo = a > c ? c : a;
+                            return As[(hi * (hi + 1)) / 2 + lo];
+                        });
+                        return;
+                    }
+                }
+                body([&](int r, int c) -> cd { return As[r * ldA + c]; });
+            } else {
+                body([&](int r, int c) -> cd { return at[r * n + c]; });
+            }
         };
         const cd* dg = diag + ir.problem * ci.dg_stride;
         // vertex list: vertex c = 2*bit[c/2] + (c&1); every index below is static except
@@ -1311,10 +1344,10 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
         if constexpr (LOOPS) {
             // lane j holds column j of B: B[i][j] = Atilde[v_{j^1}][v_{i^1}]
             const int rj = 2 * mybit + ((lane & 1) ^ 1);
-            gather([&](const cd* src, int ld) {
+            gather([&](auto&& g) {
                 static_for<0, S>([&](auto i) {
                     const int ci1 = 2 * vbit[i() >> 1] + ((i() & 1) ^ 1);
-                    hr[i()] = lane < S ? src[rj * ld + ci1] : mk(0.0, 0.0);
+                    hr[i()] = lane < S ? g(rj, ci1) : mk(0.0, 0.0);
                     return true;
                 });
             });
@@ -1356,10 +1389,10 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
         int myrow = lane;
         if constexpr (SH) {
             cd* H = ws + L::HS;
-            gather([&](const cd* src, int ld) {
+            gather([&](auto&& g) {
                 static_for<0, S>([&](auto c) {
                     const int vc = 2 * vbit[c() >> 1] + (c() & 1);
-                    if (lane < S) H[c() * S + lane] = src[vr * ld + vc];
+                    if (lane < S) H[c() * S + lane] = g(vr, vc);
                     return true;
                 });
             });
@@ -1377,10 +1410,10 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
             constexpr int K = NSK;
             cd* Hq = ws + L::HS + NsSplit<S, K>::BASE;
             if constexpr (K > 2) tc.sync();  // the previous subset's readers of the region
-            gather([&](const cd* src, int ld) {
+            gather([&](auto&& g) {
                 static_for<0, S>([&](auto c) {
                     const int vc = 2 * vbit[c() >> 1] + (c() & 1);
-                    const cd v = src[vr * ld + vc];
+                    const cd v = g(vr, vc);
                     if constexpr (c() >= 2 && c() < K) Hq[c() * 32 + lane] = v;
                     else hr[c()] = v;
                     return true;
@@ -1388,8 +1421,8 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
                 static_for<0, E>([&](auto ee) {
                     constexpr int e = decltype(ee)::value;
                     const int rv = 2 * vbit[16 + e / 2] + (e & 1);
-                    ex[e] = src[rv * ld + 2 * mybit + (lane & 1)];
-                    if (lane < E) CR[e * E + lane] = src[rv * ld + 2 * cb1 + (lane & 1)];
+                    ex[e] = g(rv, 2 * mybit + (lane & 1));
+                    if (lane < E) CR[e * E + lane] = g(rv, 2 * cb1 + (lane & 1));
                     elab[e] = 32 + e;
                     return true;
                 });
@@ -1400,10 +1433,10 @@ __global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ at
             constexpr int K = NSK;
             cd* Hq = ws + L::HS + NsSplit<S, K>::BASE;
             if constexpr (K > 2) tc.sync();  // the previous subset's readers of the region
-            gather([&](const cd* src, int ld) {
+            gather([&](auto&& g) {
                 static_for<0, S>([&](auto c) {
                     const int vc = 2 * vbit[c() >> 1] + (c() & 1);
-                    const cd v = lane < S ? src[vr * ld + vc] : mk(0.0, 0.0);
+                    const cd v = lane < S ? g(vr, vc) : mk(0.0, 0.0);
                     if constexpr (c() >= 2 && c() < K) Hq[c() * 32 + lane] = v;
                     else hr[c()] = v;
                     return true;

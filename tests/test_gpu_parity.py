@@ -364,6 +364,34 @@ def test_fast_extra_row_classes_full_class_vs_oracle(S):
     assert np.abs(got[idx] - ref).max() <= 1e-10 * scale
 
 
+@pytest.mark.parametrize("n", [52, 60])
+@pytest.mark.parametrize("symmetric", [True, False])
+def test_fast_triangular_staging_and_asymmetric_fallback(n, symmetric):
+    """The split-row NSX classes (S = 34, 36) run 12 teams per SM; where the full staged
+    Atilde no longer fits beside them the blocks stage only the lower triangle of the
+    symmetric A behind Atilde = X A, after verifying Atilde[r][c] == Atilde[c^1][r^1] bit for
+    bit.  An Atilde that is not of that form (legal at the kernel-module contract, which takes
+    any matrix) must take the global-memory gather instead and still match the oracle."""
+    A = random_symmetric(n, 4242 + n) / np.sqrt(n)
+    at, dg, nh = engine._prepare(A, False)
+    if not symmetric:
+        rng = np.random.default_rng(n)
+        at = at + 1e-3 * (rng.normal(size=at.shape) + 1j * rng.normal(size=at.shape))
+    rng = np.random.default_rng(7 * n)
+    masks = []
+    for S in (30, 32, 34, 36):
+        for _ in range(24):
+            bits = rng.choice(nh, size=S // 2, replace=False)
+            masks.append(int(sum(1 << int(b) for b in bits)))
+    masks = np.array(masks, dtype=np.uint64)
+    ref, _ = O.terms(at, dg, nh, masks, backend=1)
+    got, st = kernels.terms(at, dg, nh, masks, 1, False, arith="fast")
+    assert not st.any()
+    for k in range(4):  # per size class: terms of different classes differ by orders of magnitude
+        sl = slice(24 * k, 24 * (k + 1))
+        assert np.abs(got[sl] - ref[sl]).max() <= 1e-10 * np.abs(ref[sl]).max()
+
+
 @pytest.mark.parametrize("n", [34, 36, 38])
 def test_fast_nsx_whole_problems(n):
     """Whole problems whose largest classes run on the NSX kernel: FAST vs the bit-exact

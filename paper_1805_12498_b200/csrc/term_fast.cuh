@@ -125,7 +125,7 @@ struct FastLayout {
     // S = 28 (static-column kernel, one pivot-row and one multiplier buffer): single
     // buffers, so 16 teams and the staged Atilde of n <= 56 fit one SM's shared memory
     static constexpr bool TRIM = !SH && S == 28 && HAFB_NS;
-    // S = 34, 36 (NSX with split rows, 10-12 teams): one pivot-row buffer; the second multiplier
+    // S = 34, 36 (NSX with split rows, 12 teams): one pivot-row buffer; the second multiplier
     // buffer stays (the tensor-core charpoly stages T in this scratch and needs the room)
     static constexpr bool TRIM_PR = TRIM || (!SH && !LOOPS && (S == 34 || S == 36) && HAFB_NS);
     static constexpr int MU = PR + ((SH || (HAFB_SHFL_PIVOT && S >= 26 && !HAFB_NS)) ? 0 : TRIM_PR ? SP : 2 * SP);

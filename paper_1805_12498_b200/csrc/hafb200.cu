@@ -84,6 +84,34 @@ cudaError_t library_pool(int device, cudaMemPool_t* out) {
 // One host call: the calling thread's non-blocking stream for the device and
 // stream-ordered allocations, released (after a stream sync) when the call returns
 // on any path.
+inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// Per-host-thread pinned staging buffer for the small synchronous entry points (grown on
+// demand, at most kPinnedMax; kept for the thread's lifetime).  nullptr: use pageable copies.
+constexpr size_t kPinnedMax = 1u << 20;
+char* pinned_staging(size_t bytes) {
+    struct Buf {
+        char* p = nullptr;
+        size_t cap = 0;
+    };
+    thread_local Buf b;
+    if (bytes > kPinnedMax) return nullptr;
+    if (b.cap < bytes) {
+        if (b.p) cudaFreeHost(b.p);
+        b.p = nullptr;
+        b.cap = 0;
+        const size_t want = std::max<size_t>(bytes, 128u << 10);
+        void* q = nullptr;
+        if (cudaHostAlloc(&q, want, cudaHostAllocPortable) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        b.p = static_cast<char*>(q);
+        b.cap = want;
+    }
+    return b.p;
+}
+
 struct Call {
     cudaStream_t st = nullptr;
     std::vector<void*> bufs;
@@ -719,24 +747,43 @@ int hafb_sum_mask_range(const double* atilde, const double* diag, int n_half, ui
     if (hi < lo || hi > (1ull << n_half) || n_chunks < 1) return fail(HAFB_ERR_ARG, "bad mask range");
     const int n = 2 * n_half;
     size_t ws_bytes = mask_range_ws_bytes(n_half, (long long)(hi - lo));
+    // One pool allocation [Atilde | diag | partials | fails | workspace] and one copy each way
+    // through the thread's pinned staging buffer: a small hafnian is a few tens of
+    // microseconds of device work, so four more allocations and two more pageable copies
+    // were a quarter of its wall time.
+    const size_t at_b = sizeof(cd) * n * n, dg_b = sizeof(cd) * n, in_b = at_b + dg_b;
+    const size_t part_b = sizeof(cd) * n_chunks, fail_b = sizeof(long long) * n_chunks;
+    const size_t out_off = align_up(in_b, 256), ws_off = align_up(out_off + part_b + fail_b, 256);
     Call c;
-    cd *d_at, *d_dg, *d_part;
-    long long* d_fail;
-    void* d_ws;
+    char* base;
     CK(c.open(device));
-    CK(c.alloc(&d_at, sizeof(cd) * n * n));
-    CK(c.alloc(&d_dg, sizeof(cd) * n));
-    CK(c.alloc(&d_ws, ws_bytes));
-    CK(c.alloc(&d_part, sizeof(cd) * n_chunks));
-    CK(c.alloc(&d_fail, sizeof(long long) * n_chunks));
-    CK(cudaMemcpyAsync(d_at, atilde, sizeof(cd) * n * n, cudaMemcpyHostToDevice, c.st));
-    CK(cudaMemcpyAsync(d_dg, diag, sizeof(cd) * n, cudaMemcpyHostToDevice, c.st));
+    CK(c.alloc(&base, ws_off + ws_bytes));
+    cd* d_at = reinterpret_cast<cd*>(base);
+    cd* d_dg = reinterpret_cast<cd*>(base + at_b);
+    cd* d_part = reinterpret_cast<cd*>(base + out_off);
+    long long* d_fail = reinterpret_cast<long long*>(base + out_off + part_b);
+    char* hp = pinned_staging(std::max(in_b, part_b + fail_b));
+    if (hp) {
+        std::memcpy(hp, atilde, at_b);
+        std::memcpy(hp + at_b, diag, dg_b);
+        CK(cudaMemcpyAsync(base, hp, in_b, cudaMemcpyHostToDevice, c.st));
+    } else {
+        CK(cudaMemcpyAsync(d_at, atilde, at_b, cudaMemcpyHostToDevice, c.st));
+        CK(cudaMemcpyAsync(d_dg, diag, dg_b, cudaMemcpyHostToDevice, c.st));
+    }
     rc = enqueue_mask_range(d_at, d_dg, n_half, lo, hi, n_chunks, backend, include_loops, cap_mult,
-                            arith, d_ws, ws_bytes, d_part, d_fail, c.st);
+                            arith, base + ws_off, ws_bytes, d_part, d_fail, c.st);
     if (rc) return rc;
-    CK(cudaMemcpyAsync(partials, d_part, sizeof(cd) * n_chunks, cudaMemcpyDeviceToHost, c.st));
-    CK(cudaMemcpyAsync(fails, d_fail, sizeof(long long) * n_chunks, cudaMemcpyDeviceToHost, c.st));
-    CK(cudaStreamSynchronize(c.st));
+    if (hp) {
+        CK(cudaMemcpyAsync(hp, d_part, part_b + fail_b, cudaMemcpyDeviceToHost, c.st));
+        CK(cudaStreamSynchronize(c.st));
+        std::memcpy(partials, hp, part_b);
+        std::memcpy(fails, hp + part_b, fail_b);
+    } else {
+        CK(cudaMemcpyAsync(partials, d_part, part_b, cudaMemcpyDeviceToHost, c.st));
+        CK(cudaMemcpyAsync(fails, d_fail, fail_b, cudaMemcpyDeviceToHost, c.st));
+        CK(cudaStreamSynchronize(c.st));
+    }
     return HAFB_OK;
 }
 

@@ -97,6 +97,33 @@ def test_tree_reduce_shape():
     assert engine.tree_reduce([]) == 0
 
 
+def test_tree_reduce_matches_reference_list_form_bitwise():
+    """The array form adds the same pairs in the same association as the reference's list
+    form (engine.py:87-97), for every length (odd tails carried up) and non-finite values."""
+    def ref(values):
+        vals = [complex(v) for v in values]
+        if not vals:
+            return 0.0 + 0.0j
+        while len(vals) > 1:
+            nxt = [vals[i] + vals[i + 1] for i in range(0, len(vals) - 1, 2)]
+            if len(vals) % 2:
+                nxt.append(vals[-1])
+            vals = nxt
+        return vals[0]
+
+    rng = np.random.default_rng(11)
+    for n in list(range(0, 20)) + [31, 33, 511, 512, 513, 1000]:
+        v = (rng.normal(size=n) + 1j * rng.normal(size=n)) * 10.0 ** rng.integers(-9, 9, size=n)
+        a, b = engine.tree_reduce(v), ref(v)
+        assert np.array([a]).view(np.uint64).tolist() == np.array([b]).view(np.uint64).tolist(), n
+        assert engine.tree_reduce(list(v)) == b
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("error")
+        bad = engine.tree_reduce(np.array([np.inf, -np.inf, 1.0, 2.0 + 0j]))
+    assert np.isnan(bad.real) and bad.imag == 0.0
+
+
 def test_workload_generators():
     a3 = workloads.cfg3()
     assert a3.shape == (40, 40) and np.count_nonzero(np.triu(a3.real, 1)) == 393

@@ -470,6 +470,9 @@ __device__ __forceinline__ void fast_hessenberg(cd (&w)[S], int& myrow, const Te
 // occupancy hides the per-step serial latency).  Rows are relabelled (lane <->
 // logical row); `lm` (logical row -> lane, double-buffered) is kept for the
 // charpoly.  Same arithmetic identities as fast_hessenberg.
+#ifndef HAFB_SH_REMAP
+#define HAFB_SH_REMAP 1
+#endif
 template <int S, int W, bool LOOPS>
 __device__ __forceinline__ void smem_hessenberg(cd* H, int& myrow, const TeamCtx<W>& tc, cd* ws) {
     using L = FastLayout<S, true, LOOPS>;
@@ -540,6 +543,36 @@ __device__ __forceinline__ void smem_hessenberg(cd* H, int& myrow, const TeamCtx
         cd acc0 = mk(0.0, 0.0), acc1 = mk(0.0, 0.0);
         const cd* prow = H + wl;  // the pivot row, read in place
         int c = J + 2;
+        if constexpr (W == 64 && HAFB_SH_REMAP) {
+            // The second warp holds only E = S - 32 rows: instead of 32 - E idle lanes walking
+            // every column, its lanes split the columns -- lane l works on row 32 + l % EP for
+            // the columns J + 2 + l / EP (mod G), EP = 8 or 16 row slots, G = 32 / EP column
+            // groups -- and the groups' gemv partials meet in a butterfly.  A quarter (half) of
+            // the second warp's shared-memory traffic and instructions; same products, the
+            // partial sums associate differently (FAST).
+            if (lane >= 32) {
+                constexpr int E = S - 32, EP = E <= 8 ? 8 : 16, G = 32 / EP;
+                const int l = lane - 32, ri = l % EP, g = l / EP;
+                const int row = 32 + (ri < E ? ri : 0);
+                cd mur;
+                mur.re = __shfl_sync(0xffffffffu, mu.re, ri);
+                mur.im = __shfl_sync(0xffffffffu, mu.im, ri);
+                const bool elr = __shfl_sync(0xffffffffu, (int)elim, ri) != 0 && ri < E;
+#pragma unroll 1
+                for (int cc = J + 2 + g; cc < S; cc += G) {
+                    const cd xa = H[cc * S + row], pa = prow[cc * S], ma = mus[cc];
+                    const cd ya = f_cms(xa, mur, pa);
+                    if (ri < E) acc0 = f_cma(acc0, ma, ya);
+                    if (elr) H[cc * S + row] = ya;
+                }
+#pragma unroll
+                for (int off = EP; off < 32; off <<= 1) {
+                    acc0.re += __shfl_xor_sync(0xffffffffu, acc0.re, off);
+                    acc0.im += __shfl_xor_sync(0xffffffffu, acc0.im, off);
+                }
+                c = S;  // the pair loop below is the first warp's
+            }
+        }
 #pragma unroll 1
         for (; c + 1 < S; c += 2) {
             const cd xa = H[c * S + lane], xb = H[(c + 1) * S + lane];

@@ -102,7 +102,12 @@ static cudaError_t launch_one(const cd* at, const cd* dg, int n_half, const Clas
         if (!stage) return launch_one<S, L, SPEC, LEVEL + 1>(at, dg, n_half, ci, terms, status, st, sms, cap);
     }
     const size_t smem = base_smem + (stage == 1 ? a_bytes : stage == 2 ? tri_bytes : 0);
-    auto kern = fast_term_kernel<S, L, SH, NT, SPEC>;
+    // 64-lane shared-memory classes that fill the GPU: the register-capped instantiation
+    // (6 teams per SM instead of 5)
+    void (*kern)(const cd*, const cd*, int, ClassItems, cd*, int8_t*, int, int) = fast_term_kernel<S, L, SH, NT, SPEC>;
+    if constexpr (sh_capped_ok(S, SH, NT) && !SPEC) {
+        if (ci.n_items >= 4LL * HAFB_SH_MINB * sms) kern = fast_term_kernel<S, L, SH, NT, SPEC, HAFB_SH_MINB>;
+    }
     // smem depends on n (the staged Atilde): the attribute is the size-independent
     // opt-in maximum, so host threads launching different n never race on it
     int occ = 1;

@@ -1216,8 +1216,20 @@ struct FastTeam {
 
 // SPEC: the spectral backend (qr_fast.cuh: shifted QR on the same packed Hessenberg
 // form, power sums) instead of the charpoly; cap_mult bounds its sweeps
-template <int S, bool LOOPS, bool SH, int NT = kFastThreads, bool SPEC = false>
-__global__ void __launch_bounds__(NT) fast_term_kernel(const cd* __restrict__ atilde,
+// minimum resident blocks per SM the register allocation must allow: the 64-lane
+// shared-memory classes (one team per 64-thread block) are latency-bound at the 5 teams
+// their ~240 registers leave.  Up to S = 42 shared memory holds 6 teams, so the kernel is
+// capped at 168 registers (332 B of spills at S = 40): S = 40..44 at n = 56 571 -> 524 ms.
+// 7 blocks (128 registers, 1.3-4 KB of spills) measured slower.
+// (the launcher picks the capped instantiation only for classes that fill 6 blocks per SM:
+// a class of a few waves is one serial chain per team, and the spills lengthen it)
+#ifndef HAFB_SH_MINB
+#define HAFB_SH_MINB 6
+#endif
+constexpr bool sh_capped_ok(int S, bool sh, int nt) { return sh && nt == 64 && S <= 42; }
+
+template <int S, bool LOOPS, bool SH, int NT = kFastThreads, bool SPEC = false, int MINB = 1>
+__global__ void __launch_bounds__(NT, MINB) fast_term_kernel(const cd* __restrict__ atilde,
                                                                  const cd* __restrict__ diag,
                                                                  int n_half, ClassItems ci,
                                                                  cd* __restrict__ terms,

@@ -1228,7 +1228,7 @@ struct FastTeam {
 #endif
 constexpr bool sh_capped_ok(int S, bool sh, int nt) { return sh && nt == 64 && S <= 42; }
 
-template <int S, bool LOOPS, bool SH, int NT = kFastThreads, bool SPEC = false, int MINB = 1>
+template <int S, bool LOOPS, bool SH, int NT = kFastThreads, bool SPEC = false, int MINB = 0>
 __global__ void __launch_bounds__(NT, MINB) fast_term_kernel(const cd* __restrict__ atilde,
                                                                  const cd* __restrict__ diag,
                                                                  int n_half, ClassItems ci,

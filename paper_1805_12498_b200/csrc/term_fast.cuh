@@ -1196,7 +1196,7 @@ constexpr int ns_split_k(int S, bool loops, bool sh, int nt) {
 // split-row bound of the NSX classes (nsx_hessenberg) in blocks of 352..384 threads (11-12
 // teams, <= 168 registers): columns 2..K-1 of the lane rows in shared memory; 2 = no split
 #ifndef HAFB_NSX_K34
-#define HAFB_NSX_K34 10
+#define HAFB_NSX_K34 12
 #endif
 #ifndef HAFB_NSX_K36
 #define HAFB_NSX_K36 20
@@ -1244,7 +1244,10 @@ __global__ void __launch_bounds__(NT, MINB) fast_term_kernel(const cd* __restric
     #ifndef HAFB_PSYNC_NS
 #define HAFB_PSYNC_NS 0
 #endif
-    constexpr bool PSYNC = NT > kFastThreads && (NSX || (HAFB_PSYNC && (!ns_variant(S) || HAFB_PSYNC_NS)));
+#ifndef HAFB_PSYNC_NSX
+#define HAFB_PSYNC_NSX 1
+#endif
+    constexpr bool PSYNC = NT > kFastThreads && ((NSX && HAFB_PSYNC_NSX) || (HAFB_PSYNC && (!ns_variant(S) || HAFB_PSYNC_NS)));
     constexpr int W = FastTeam<S, LOOPS, SH>::W;
     constexpr int TPB = NT / W;
     constexpr int NSK = NSX ? nsx_split_k(S, NT) : ns_split_k(S, LOOPS, SH, NT);

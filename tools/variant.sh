@@ -14,5 +14,6 @@ for S in "$@"; do
     -c paper_1805_12498_b200/csrc/fast_inst.cu -o $OUT/fast_$SS.o 2> $OUT/fast_$SS.log &
 done
 wait
+for S in "$@"; do SS=$(printf %02d $S); if grep -q "error" $OUT/fast_$SS.log; then echo "COMPILE FAILED for S=$S:"; grep -m3 "error" $OUT/fast_$SS.log; exit 1; fi; done
 for S in "$@"; do SS=$(printf %02d $S); python tools/ptxas_regs.py "false, false, [0-9]+, false" < $OUT/fast_$SS.log; done
 nvcc -gencode arch=compute_100a,code=sm_100a --shared -o build_variants/$NAME.so $OUT/*.o && echo built build_variants/$NAME.so

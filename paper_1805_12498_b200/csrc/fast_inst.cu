@@ -69,7 +69,7 @@ constexpr int threads_for(int S, bool loops) {
 // 2 % slower than the unsplit kernel).  The unsplit 256-thread kernel (8 teams) is the last
 // level and the FAST spectral configuration.
 constexpr int nsx_threads(int S, bool spec, int level) {
-    if (spec || nsx_split_k(S, 384) <= 2) return HAFB_NSX_THREADS;
+    if (spec || S == 38 || nsx_split_k(S, 384) <= 2) return HAFB_NSX_THREADS;
     return level == 0 ? 384 : level == 1 ? 352 : HAFB_NSX_THREADS;
 }
 

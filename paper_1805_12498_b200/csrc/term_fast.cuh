@@ -1182,12 +1182,18 @@ namespace hafb {
 // blocks of >= 512 threads (16 teams, <= 128 registers) keep HAFB_NS_KEEP columns
 // (K..S-1) of the lane's row in registers, columns 2..K-1 in shared memory
 #ifndef HAFB_NS_KEEP
-#define HAFB_NS_KEEP 16
+#define HAFB_NS_KEEP 18
 #endif
 #ifndef HAFB_NS_SPLIT_LO
 #define HAFB_NS_SPLIT_LO 24
 #endif
+#ifndef HAFB_NS_K12T
+#define HAFB_NS_K12T 2
+#endif
 constexpr int ns_split_k(int S, bool loops, bool sh, int nt) {
+    // S = 30, 32 at their 12 teams (384 threads, 168 registers): HAFB_NS_K12T split columns
+    // only relieve the register allocation
+    if (ns_variant(S) && !loops && !sh && (S == 30 || S == 32) && nt == 384) return HAFB_NS_K12T;
     return (ns_variant(S) && !loops && !sh && S >= HAFB_NS_SPLIT_LO && S <= 32 && nt >= 512 && S - HAFB_NS_KEEP > 2)
                ? S - HAFB_NS_KEEP
                : 2;
@@ -1202,10 +1208,12 @@ constexpr int ns_split_k(int S, bool loops, bool sh, int nt) {
 #define HAFB_NSX_K36 20
 #endif
 #ifndef HAFB_NSX_K38
-#define HAFB_NSX_K38 2
+#define HAFB_NSX_K38 14
 #endif
 constexpr int nsx_split_k(int S, int nt) {
-    return nt < 320 ? 2 : S == 34 ? HAFB_NSX_K34 : S == 36 ? HAFB_NSX_K36 : S == 38 ? HAFB_NSX_K38 : 2;
+    // S = 38 stays at 8 teams (its workspace fits 10 at most): a split there only relieves
+    // the 255-register allocation
+    return S == 38 ? HAFB_NSX_K38 : nt < 320 ? 2 : S == 34 ? HAFB_NSX_K34 : S == 36 ? HAFB_NSX_K36 : 2;
 }
 
 template <int S, bool LOOPS, bool SH>

@@ -1187,6 +1187,9 @@ namespace hafb {
 #ifndef HAFB_NS_SPLIT_LO
 #define HAFB_NS_SPLIT_LO 24
 #endif
+#ifndef HAFB_NS_KEEP_SMALL
+#define HAFB_NS_KEEP_SMALL 16
+#endif
 #ifndef HAFB_NS_K12T
 #define HAFB_NS_K12T 2
 #endif
@@ -1195,8 +1198,12 @@ constexpr int ns_split_k(int S, bool loops, bool sh, int nt) {
     // only relieve the register allocation (measured: K = 6 -0.07 %, K = 10 +0.06 % per n = 52
     // step; left off)
     if (ns_variant(S) && !loops && !sh && (S == 30 || S == 32) && nt == 384) return HAFB_NS_K12T;
-    return (ns_variant(S) && !loops && !sh && S >= HAFB_NS_SPLIT_LO && S <= 32 && nt >= 512 && S - HAFB_NS_KEEP > 2)
-               ? S - HAFB_NS_KEEP
+    // S <= 22 (already 16 teams at 128 registers) would keep HAFB_NS_KEEP_SMALL columns
+    // (HAFB_NS_SPLIT_LO = 20): the split there only relieves the register allocation --
+    // measured -5 ms per n = 52 step but +2 % on the 4096-matrix n = 24 batch, so it is off
+    const int keep = S <= 22 ? HAFB_NS_KEEP_SMALL : HAFB_NS_KEEP;
+    return (ns_variant(S) && !loops && !sh && S >= HAFB_NS_SPLIT_LO && S <= 32 && nt >= 512 && S - keep > 2)
+               ? S - keep
                : 2;
 }
 
